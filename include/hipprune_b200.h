@@ -1,0 +1,182 @@
+/*
+ * hipprune_b200 — C ABI of the B200-native InfiniteHiP attention hot path.
+ *
+ * Plain pointers and sizes only (no torch / C++ types). All device pointers
+ * are caller-owned; no entry point allocates on the hot path. Every call is
+ * asynchronous on the given cudaStream_t (passed as void*) and re-entrant per
+ * stream. Status codes map 1:1 onto the reference's exception types
+ * (SURVEY.md §8(b)); hp_last_error() returns the thread's last message.
+ *
+ * Each entry point names the reference interface it replaces
+ * (paths relative to /root/reference/proj).
+ *
+ * Layouts
+ *   q        fp32 [n_q_heads][q_rows][d]          (decode: q_rows == 1)
+ *   K/V pool [num_slots][n_kv][page_size][d]      of HP_F32 or HP_BF16
+ *   page     covers page_size consecutive tokens of all kv heads of one layer
+ *            (kv_store.cpp:50-56); page_table maps page -> slot, -1 = not
+ *            resident (read from the host tier instead, a cache miss).
+ *   lists    int32 token indices, [n_masks][n_blocks][stride] + int32 counts.
+ *   GQA      q-head h reads kv-head h / (n_q_heads / n_kv); mask m pools the
+ *            q-heads [m*hpm, (m+1)*hpm) (one reference call per KV group).
+ */
+#ifndef HIPPRUNE_B200_H
+#define HIPPRUNE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes == reference exception types */
+enum hp_status {
+    HP_OK = 0,
+    HP_CONTRACT_VIOLATION = 1, /* hipprune::ContractViolation (errors.hpp:8-10)  */
+    HP_INVALID_ARGUMENT = 2,   /* std::invalid_argument                         */
+    HP_OUT_OF_RANGE = 3,       /* std::out_of_range                             */
+    HP_LOGIC_ERROR = 4,        /* std::logic_error                              */
+    HP_RUNTIME_ERROR = 5,      /* std::runtime_error / CUDA failure             */
+    HP_PARTIAL_COMMIT = 6      /* hipprune::PartialCommitError (kv_store.hpp:41) */
+};
+
+enum hp_dtype { HP_F32 = 0, HP_BF16 = 1 };
+
+/* RoPE policy ids (rope_policy.hpp:11) */
+enum hp_rope_policy { HP_ROPE_CHUNK_INDEXED = 0, HP_ROPE_RELATIVE = 1, HP_ROPE_STREAMING = 2 };
+
+const char* hp_last_error(void);
+int hp_version(void);
+/* 1 when a CUDA device is usable; product calls fail with HP_RUNTIME_ERROR otherwise. */
+int hp_device_available(void);
+
+/* Device-resident paged KV of one layer (replaces KeySource / KvView,
+ * key_source.hpp:13-18, kv_store.cpp:160-200). */
+typedef struct hp_kv_view {
+    const void* k_pool;          /* [num_slots][n_kv][page_size][d]                    */
+    const void* v_pool;          /* same layout; may be NULL for key-only (Mask bank)  */
+    const void* k_host;          /* optional device-mapped host tier [num_pages][...]  */
+    const void* v_host;
+    const int32_t* page_table;   /* [num_pages] page -> slot (-1 miss); NULL = identity */
+    uint8_t* touched;            /* optional [num_pages] flags: 1 hit, 2 miss (phase)  */
+    int32_t num_pages;
+    int32_t page_size;
+    int32_t n_kv;
+    int32_t d;
+    int32_t dtype;               /* hp_dtype */
+    int32_t t_kv;                /* valid tokens (bounds) */
+} hp_kv_view;
+
+/* RoPE context (StageContext, pruning.hpp:55-63 + RopePolicySet, rope_policy.hpp:24-34).
+ * cos/sin: device fp32 [rope_max][d/2], built by hp_build_rope_table (bit-identical
+ * to build_rope_table, tensor.cpp:30-59). */
+typedef struct hp_rope_ctx {
+    const float* cos_tab;
+    const float* sin_tab;
+    int64_t rope_max;
+    int32_t extension;           /* RopePolicySet::extension_enabled                  */
+    int32_t early_cutoff;        /* early_layer_cutoff (layers are 1-based)            */
+    int32_t early_policy;        /* hp_rope_policy for layers <= cutoff                */
+    int32_t late_policy;         /* hp_rope_policy for layers > cutoff                 */
+    int32_t layer;               /* 1-based layer (StageContext::layer)                */
+    int32_t pad_;
+} hp_rope_ctx;
+
+/* Host helper: the reference's double-precision table, cast to float. */
+int hp_build_rope_table(int64_t max_pos, int32_t d, float theta, float* cos_out, float* sin_out);
+
+/* ------------------------------------------------------------------------ *
+ * One pruning stage over a batch of (mask, query-block) index lists.
+ * Replaces run_pruning_stage + select_rep + block_scores
+ * (pruning.cpp:69-98,153-200; tensor.cpp:88-114) with index-exact results.
+ * ------------------------------------------------------------------------ */
+typedef struct hp_stage_args {
+    /* stage S = (b_q, l_c, k)  (StageConfig, pruning.hpp:15-21) */
+    int32_t query_block;
+    int32_t chunk_size;
+    int32_t keep;
+    /* batch geometry */
+    int32_t n_masks;             /* independent pooled masks (KV groups)               */
+    int32_t heads_per_mask;      /* q-heads pooled into one chunk score                */
+    int32_t n_q_heads;
+    int32_t n_blocks;            /* query blocks per mask                              */
+    int32_t q_rows;              /* rows of q per head (T_q)                           */
+    const float* q;              /* [n_q_heads][q_rows][d]                             */
+    int64_t query_offset;        /* absolute position of q row 0 (T_kv - T_q)          */
+    int32_t stream_tokens;       /* StageContext::stream_tokens                        */
+    int32_t max_chunks;          /* upper bound on chunks per list (grid sizing)       */
+    /* input: range mode (in_list == NULL): list(m,b) = [in_start[mb], in_start[mb]+in_count[mb])
+     *        list mode: in_list[mb*in_stride + i], i < in_count[mb] (sorted, unique) */
+    const int32_t* in_list;
+    const int32_t* in_start;
+    const int32_t* in_count;
+    int64_t in_stride;
+    /* output: out_list[mb*out_stride + i], out_count[mb]; out_stride >= keep (or >= in for identity) */
+    int32_t* out_list;
+    int32_t* out_count;
+    int64_t out_stride;
+    /* workspace: >= hp_stage_workspace_bytes() bytes of device memory */
+    void* workspace;
+    size_t workspace_bytes;
+    hp_kv_view keys;
+    hp_rope_ctx rope;
+} hp_stage_args;
+
+size_t hp_stage_workspace_bytes(int32_t n_lists, int32_t max_chunks, int32_t keep, int32_t chunk_size);
+int hp_prune_stage(const hp_stage_args* args, void* stream);
+
+/* Sub-block remap between stages with different b_q (pruning.cpp:285-303):
+ * next(m2) = { idx in parent(min(m2/ratio, nb-1)) : idx < middle_upper(bq_next, m2) }. */
+int hp_remap_blocks(const int32_t* in_list, const int32_t* in_count, int64_t in_stride,
+                    int32_t n_masks, int32_t n_blocks, int32_t bq, int32_t bq_next, int32_t t_q,
+                    int64_t query_offset, int32_t stream_tokens, int32_t* out_list,
+                    int32_t* out_count, int64_t out_stride, void* stream);
+
+/* Per-row selected index list (selected_indices, sparse_attention.cpp:95-112):
+ * sinks [0,min(n_sink,pos+1)) ++ mask∩[sink_end,stream_begin) ++ [stream_begin,pos]. */
+int hp_selected_indices(const int32_t* mask_list, const int32_t* mask_count, int64_t mask_stride,
+                        int32_t n_masks, int32_t n_rows, int32_t block_size, int64_t query_offset,
+                        int32_t sink_tokens, int32_t stream_tokens, int32_t* sel_list,
+                        int32_t* sel_count, int64_t sel_stride, void* stream);
+
+/* ------------------------------------------------------------------------ *
+ * Block-sparse attention over explicit per-row selected lists: split-K with
+ * online softmax + log-sum-exp combine. Replaces attention_row +
+ * softmax_weighted_sum (sparse_attention.cpp:15-60) for decode and for
+ * block_sparse_attention (sparse_attention.cpp:114-145) row by row.
+ * ------------------------------------------------------------------------ */
+typedef struct hp_bsa_args {
+    int32_t n_q_heads;
+    int32_t heads_per_mask;      /* q-head h uses the lists of mask h / heads_per_mask  */
+    int32_t n_rows;              /* query rows per head                                  */
+    const float* q;              /* [n_q_heads][n_rows][d]                              */
+    int64_t query_offset;        /* position of row r = query_offset + r                 */
+    const int32_t* sel_list;     /* [n_masks][n_rows][sel_stride]                       */
+    const int32_t* sel_count;    /* [n_masks][n_rows]                                   */
+    int64_t sel_stride;
+    int32_t max_sel;             /* upper bound on counts (grid sizing)                 */
+    float* out;                  /* [n_q_heads][n_rows][d] fp32                          */
+    /* optional per-split partials for a cross-shard merge (NULL = combine in place):
+     * m, l [n_q_heads][n_rows], o [n_q_heads][n_rows][d] — the shard's LSE triple */
+    float* part_m;
+    float* part_l;
+    float* part_o;
+    void* workspace;
+    size_t workspace_bytes;
+    hp_kv_view kv;
+    hp_rope_ctx rope;            /* extension on => streaming positions (BSA policy)    */
+} hp_bsa_args;
+
+size_t hp_bsa_workspace_bytes(int32_t n_q_heads, int32_t n_rows, int32_t max_sel, int32_t d);
+int hp_bsa(const hp_bsa_args* args, void* stream);
+
+/* Log-sum-exp merge of per-shard (m, l, o) partials (C5 sequence sharding):
+ * m, l [n_shards][n]; o [n_shards][n][d] -> out [n][d]. */
+int hp_lse_merge(const float* m, const float* l, const float* o, int32_t n_shards, int32_t n,
+                 int32_t d, float* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HIPPRUNE_B200_H */

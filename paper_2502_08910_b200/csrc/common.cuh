@@ -1,0 +1,124 @@
+// Shared device helpers for the hipprune_b200 kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "hipprune_b200.h"
+
+namespace hpk {
+
+constexpr int kWarp = 32;
+
+__host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+__host__ __device__ __forceinline__ int64_t max64(int64_t a, int64_t b) { return a > b ? a : b; }
+
+// ---- element access ---------------------------------------------------------
+// bf16 -> fp32 is exact (bit shift); every K/V element enters the fp32 arithmetic
+// with the value the reference sees after the same bf16 rounding of its inputs.
+__device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+
+template <typename T> struct Elem;
+template <> struct Elem<float> { static constexpr int bytes = 4; static constexpr int id = HP_F32; };
+struct bf16_t { uint16_t bits; };
+template <> struct Elem<bf16_t> { static constexpr int bytes = 2; static constexpr int id = HP_BF16; };
+
+__device__ __forceinline__ float load_elem(const float* p, int i) { return p[i]; }
+__device__ __forceinline__ float load_elem(const bf16_t* p, int i) {
+    return __uint_as_float(static_cast<uint32_t>(p[i].bits) << 16);
+}
+
+// ---- paged KV resolution (KvView::key_row, kv_store.cpp:160-163) ------------------
+// page = token / page_size covers all kv heads of the layer (kv_store.cpp:50-56).
+// Non-resident pages (slot < 0) resolve to the device-mapped host tier: the read is
+// served over the host link and recorded as a miss for the step-end commit.
+__device__ __forceinline__ const char* kv_row_ptr(const hp_kv_view& v, const void* pool,
+                                                  const void* host, int kv, int64_t tok,
+                                                  int elem_bytes) {
+    const int64_t page = tok / v.page_size;
+    const int64_t off = tok - page * v.page_size;
+    int64_t slot = v.page_table ? static_cast<int64_t>(v.page_table[page]) : page;
+    const bool hit = slot >= 0;
+    if (v.touched) {
+        const uint8_t flag = hit ? 1 : 2;
+        if (v.touched[page] != flag) v.touched[page] = flag;
+    }
+    if (hit) {
+        return static_cast<const char*>(pool) +
+               (((slot * v.n_kv + kv) * v.page_size + off) * v.d) * elem_bytes;
+    }
+    return static_cast<const char*>(host) +
+           (((page * v.n_kv + kv) * v.page_size + off) * v.d) * elem_bytes;
+}
+
+// ---- RoPE policy (rope_policy.cpp:18-57) -----------------------------------------
+__device__ __forceinline__ int pruning_policy(const hp_rope_ctx& r) {
+    return r.layer > r.early_cutoff ? r.late_policy : r.early_policy;
+}
+__device__ __forceinline__ int64_t rope_q_position(const hp_rope_ctx& r, int64_t qpos,
+                                                   int64_t stream, int64_t chunk_count) {
+    if (pruning_policy(r) == HP_ROPE_RELATIVE) return stream + 1;
+    const int64_t cap = chunk_count + stream;  // ChunkIndexed
+    return qpos < cap ? qpos : cap;
+}
+__device__ __forceinline__ int64_t rope_k_position(const hp_rope_ctx& r, int branch,
+                                                   int64_t chunk_index) {
+    if (pruning_policy(r) == HP_ROPE_RELATIVE) return branch - 1;
+    return chunk_index;
+}
+
+// ---- ordered keys for top-k --------------------------------------------------------
+// Monotone map float -> uint32 (ascending). -0.0 is folded onto +0.0 so that equal
+// scores compare equal exactly as the reference's operator> does (pruning.cpp:189-190).
+__device__ __forceinline__ uint32_t order_key(float s) {
+    if (s == 0.0f) s = 0.0f;
+    const uint32_t u = __float_as_uint(s);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+// ---- block scans ---------------------------------------------------------------------
+template <int kThreads>
+__device__ __forceinline__ int block_exclusive_scan(int v, int* smem_warp, int* total) {
+    static_assert(kThreads % kWarp == 0 && kThreads <= 1024, "block size");
+    constexpr int kWarps = kThreads / kWarp;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) smem_warp[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        int t = lane < kWarps ? smem_warp[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += y;
+        }
+        if (lane < kWarps) smem_warp[lane] = t;  // inclusive warp totals
+    }
+    __syncthreads();
+    const int base = w ? smem_warp[w - 1] : 0;
+    *total = smem_warp[kWarps - 1];
+    __syncthreads();
+    return base + x - v;
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
+}  // namespace hpk
+
+// host-side error plumbing shared by the C-ABI translation units
+namespace hph {
+int set_error(int code, const char* fmt, ...);
+int check_cuda(cudaError_t e, const char* what);
+}  // namespace hph

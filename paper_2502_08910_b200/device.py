@@ -1,0 +1,367 @@
+"""Device-side orchestration of the hot path over the C ABI.
+
+torch is used only for device memory and streams; every byte of compute runs
+in the sm_100a kernels of ``_lib/libhipprune_b200.so``. There is no CPU path:
+without the library or a CUDA device the calls raise.
+
+Mapping to the reference (paths relative to /root/reference/proj):
+  PagedKV              KeySource / KvView over a paged layer (key_source.hpp:13-18,
+                       kv_store.cpp:50-56,160-200) — pages of `page_size` tokens
+                       covering all kv heads, pool layout [slot][n_kv][page][d]
+  RopeTable            build_rope_table (tensor.cpp:30-59), uploaded
+  build_mask           build_mask (pruning.cpp:202-313)
+  prune_stage          run_pruning_stage (pruning.cpp:153-200)
+  selected_indices     selected_indices (sparse_attention.cpp:95-112)
+  bsa                  attention_row / block_sparse_attention (sparse_attention.cpp:33-145)
+  DecodeLayer          the per-layer body of DecodeEngine::step (decode.cpp:225-273)
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _capi
+from ._capi import BsaArgs, KvView, RopeCtx, StageArgs, check, lib
+
+_DT = {torch.float32: _capi.HP_F32, torch.bfloat16: _capi.HP_BF16}
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _stream(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def require_cuda() -> None:
+    lib()
+    if not torch.cuda.is_available() or not lib().hp_device_available():
+        raise RuntimeError("hipprune_b200: no CUDA device — the B200 path has no CPU fallback")
+
+
+def ceil_div(a: int, b: int) -> int:
+    return (a + b - 1) // b
+
+
+# ----------------------------------------------------------------------------- KV
+class PagedKV:
+    """Paged K/V of one layer resident in HBM (identity page table) or cached.
+
+    k, v: [n_kv, T, d] tensors. Pool layout [num_slots][n_kv][page_size][d].
+    ``capacity`` (tokens) reserves pages for decode appends.
+    """
+
+    def __init__(self, k: torch.Tensor, v: torch.Tensor | None, *, page_size: int = 64,
+                 dtype: torch.dtype = torch.bfloat16, capacity: int | None = None,
+                 device="cuda"):
+        assert k.dim() == 3
+        self.n_kv, t, self.d = k.shape
+        self.page_size = page_size
+        self.dtype = dtype
+        self.t_kv = t
+        cap = max(capacity or t, t)
+        self.num_pages = ceil_div(cap, page_size)
+        self.k_pool = self._pack(k, device)
+        self.v_pool = self._pack(v, device) if v is not None else None
+        self.page_table = None
+        self.touched = None
+
+    def _pack(self, x: torch.Tensor, device) -> torch.Tensor:
+        n_kv, t, d = x.shape
+        ps = self.page_size
+        pool = torch.zeros(self.num_pages, n_kv, ps, d, dtype=self.dtype, device=device)
+        full = t // ps
+        xd = x.to(device=device, dtype=self.dtype)
+        if full:
+            pool[:full].copy_(xd[:, : full * ps].reshape(n_kv, full, ps, d).permute(1, 0, 2, 3))
+        rem = t - full * ps
+        if rem:
+            pool[full, :, :rem].copy_(xd[:, full * ps:])
+        return pool
+
+    def append(self, k_row: torch.Tensor, v_row: torch.Tensor | None = None) -> None:
+        """Append one token's K/V rows [n_kv, d] (DecodeEngine::step, decode.cpp:202-208)."""
+        t = self.t_kv
+        page, off = divmod(t, self.page_size)
+        if page >= self.num_pages:
+            raise IndexError("PagedKV: capacity exhausted")
+        self.k_pool[page, :, off].copy_(k_row)
+        if v_row is not None and self.v_pool is not None:
+            self.v_pool[page, :, off].copy_(v_row)
+        self.t_kv = t + 1
+
+    def view(self, t_kv: int | None = None) -> KvView:
+        return KvView(k_pool=_ptr(self.k_pool), v_pool=_ptr(self.v_pool), k_host=None,
+                      v_host=None, page_table=_ptr(self.page_table), touched=_ptr(self.touched),
+                      num_pages=self.num_pages, page_size=self.page_size, n_kv=self.n_kv,
+                      d=self.d, dtype=_DT[self.dtype], t_kv=t_kv if t_kv is not None else self.t_kv)
+
+
+# --------------------------------------------------------------------------- RoPE
+class RopeTable:
+    """build_rope_table (tensor.cpp:30-59) computed on the host in double and uploaded."""
+
+    def __init__(self, max_pos: int, d: int, theta: float = 10000.0, device="cuda"):
+        half = d // 2
+        cos = np.empty((max_pos, half), np.float32)
+        sin = np.empty((max_pos, half), np.float32)
+        check(lib().hp_build_rope_table(max_pos, d, theta, cos.ctypes.data, sin.ctypes.data))
+        self.max_pos, self.d = max_pos, d
+        self.cos_host, self.sin_host = cos, sin
+        self.cos = torch.from_numpy(cos).to(device)
+        self.sin = torch.from_numpy(sin).to(device)
+
+
+@dataclass
+class RopePolicy:
+    """RopePolicySet (rope_policy.hpp:24-34); pruning layer is 1-based."""
+    extension: bool = False
+    early_cutoff: int = 3
+    early_policy: int = _capi.HP_ROPE_CHUNK_INDEXED
+    late_policy: int = _capi.HP_ROPE_RELATIVE
+
+    def ctx(self, layer1: int, table: RopeTable | None) -> RopeCtx:
+        if self.extension and table is None:
+            raise ValueError("RopePolicy: extension enabled without a rope table")
+        return RopeCtx(cos_tab=_ptr(table.cos) if (table is not None and self.extension) else None,
+                       sin_tab=_ptr(table.sin) if (table is not None and self.extension) else None,
+                       rope_max=table.max_pos if table is not None else 0,
+                       extension=int(self.extension), early_cutoff=self.early_cutoff,
+                       early_policy=self.early_policy, late_policy=self.late_policy,
+                       layer=layer1, pad_=0)
+
+
+# ------------------------------------------------------------------------- stages
+class Workspace:
+    """Grow-only device scratch (allocated outside the hot path)."""
+
+    def __init__(self, device="cuda"):
+        self.buf = torch.empty(0, dtype=torch.uint8, device=device)
+
+    def get(self, nbytes: int) -> torch.Tensor:
+        if self.buf.numel() < nbytes:
+            self.buf = torch.empty(nbytes, dtype=torch.uint8, device=self.buf.device)
+        return self.buf
+
+
+def prune_stage(stage, q: torch.Tensor, kv: PagedKV, *, n_masks: int, n_blocks: int = 1,
+                in_list: torch.Tensor | None = None, in_start: torch.Tensor | None = None,
+                in_count: torch.Tensor, in_stride: int = 0, max_chunks: int,
+                out_list: torch.Tensor, out_count: torch.Tensor, query_offset: int,
+                stream_tokens: int, layer1: int, policy: RopePolicy, rope: RopeTable | None,
+                ws: Workspace, stream=None) -> None:
+    """One pruning stage over n_masks x n_blocks lists (run_pruning_stage, pruning.cpp:153-200)."""
+    bq, lc, keep = stage
+    hq, q_rows, _ = q.shape
+    need = lib().hp_stage_workspace_bytes(n_masks * n_blocks, max(1, max_chunks), keep, lc)
+    w = ws.get(need)
+    a = StageArgs(query_block=bq, chunk_size=lc, keep=keep, n_masks=n_masks,
+                  heads_per_mask=hq // n_masks, n_q_heads=hq, n_blocks=n_blocks, q_rows=q_rows,
+                  q=_ptr(q), query_offset=query_offset, stream_tokens=stream_tokens,
+                  max_chunks=max_chunks, in_list=_ptr(in_list), in_start=_ptr(in_start),
+                  in_count=_ptr(in_count), in_stride=in_stride, out_list=_ptr(out_list),
+                  out_count=_ptr(out_count), out_stride=out_list.shape[-1], workspace=_ptr(w),
+                  workspace_bytes=w.numel(), keys=kv.view(), rope=policy.ctx(layer1, rope))
+    check(lib().hp_prune_stage(C.byref(a), C.c_void_p(_stream(stream))))
+
+
+def build_mask(q: torch.Tensor, kv: PagedKV, stages, *, sink: int, stream_tokens: int,
+               t_kv: int | None = None, layer0: int = 0, policy: RopePolicy | None = None,
+               rope: RopeTable | None = None, n_masks: int = 1, ws: Workspace | None = None,
+               stream=None):
+    """build_mask (pruning.cpp:202-313) on the device.
+
+    q: fp32 [n_q_heads, T_q, d] on the device. Returns (lists [n_masks, n_blocks, keep],
+    counts [n_masks, n_blocks], trace list of (list, count) per stage for the last block,
+    block_size, query_offset).
+    """
+    require_cuda()
+    policy = policy or RopePolicy()
+    ws = ws or Workspace(q.device)
+    hq, t_q, d = q.shape
+    t_kv = kv.t_kv if t_kv is None else t_kv
+    if t_q == 0 or t_q > t_kv:
+        raise ValueError("build_mask: workload query length inconsistent")
+    for bq, lc, keep in stages:
+        if bq <= 0 or lc <= 0:
+            raise ValueError("StageConfig: b_q and l_c must be >= 1")
+        if keep <= 0 or keep % lc:
+            raise ValueError("StageConfig: k must be a positive multiple of l_c")
+    if not stages:
+        raise ValueError("PruningPlan: no stages")
+    for i in range(1, len(stages)):
+        if stages[i][0] > stages[i - 1][0] or stages[i - 1][0] % stages[i][0]:
+            raise ValueError("PruningPlan: successive b_q must be non-increasing and divisible")
+        if stages[i][2] > stages[i - 1][2]:
+            raise ValueError("PruningPlan: k must be non-increasing across stages")
+    offset = t_kv - t_q
+    dev = q.device
+    bq = stages[0][0]
+    nb = ceil_div(t_q, bq)
+    starts = np.full((n_masks, nb), sink, np.int32)
+    counts = np.zeros((n_masks, nb), np.int32)
+    for m in range(nb):
+        end = offset + min((m + 1) * bq, t_q)
+        upper = end - stream_tokens if end > stream_tokens else 0
+        counts[:, m] = max(0, upper - sink)
+    in_start = torch.from_numpy(starts).to(dev)
+    in_count = torch.from_numpy(counts).to(dev)
+    in_list = None
+    in_stride = 0
+    max_in = int(counts.max()) if counts.size else 0
+    trace = []
+    rope_ctx_layer = layer0 + 1
+    for si, (bq, lc, keep) in enumerate(stages):
+        out_list = torch.empty((n_masks, nb, keep), dtype=torch.int32, device=dev)
+        out_count = torch.empty((n_masks, nb), dtype=torch.int32, device=dev)
+        prune_stage((bq, lc, keep), q, kv, n_masks=n_masks, n_blocks=nb, in_list=in_list,
+                    in_start=in_start, in_count=in_count, in_stride=in_stride,
+                    max_chunks=ceil_div(max_in, lc), out_list=out_list, out_count=out_count,
+                    query_offset=offset, stream_tokens=stream_tokens, layer1=rope_ctx_layer,
+                    policy=policy, rope=rope, ws=ws, stream=stream)
+        trace.append((out_list[:, nb - 1], out_count[:, nb - 1]))
+        in_list, in_count, in_start, in_stride = out_list, out_count, None, keep
+        max_in = keep
+        if si + 1 < len(stages) and stages[si + 1][0] != bq:
+            bq_next = stages[si + 1][0]
+            nb2 = ceil_div(t_q, bq_next)
+            nl = torch.empty((n_masks, nb2, keep), dtype=torch.int32, device=dev)
+            nc = torch.empty((n_masks, nb2), dtype=torch.int32, device=dev)
+            check(lib().hp_remap_blocks(_ptr(out_list), _ptr(out_count), keep, n_masks, nb, bq,
+                                        bq_next, t_q, offset, stream_tokens, _ptr(nl), _ptr(nc),
+                                        keep, C.c_void_p(_stream(stream))))
+            in_list, in_count, nb = nl, nc, nb2
+    return in_list, in_count, trace, stages[-1][0], offset
+
+
+def selected_indices(mask_list: torch.Tensor, mask_count: torch.Tensor, *, n_rows: int,
+                     block_size: int, query_offset: int, sink: int, stream_tokens: int,
+                     sel_stride: int | None = None, out=None, stream=None):
+    """Per-row selected lists (selected_indices, sparse_attention.cpp:95-112)."""
+    n_masks = mask_list.shape[0]
+    cap = mask_list.shape[-1]
+    sel_stride = sel_stride or (sink + cap + stream_tokens + 1)
+    if out is None:
+        sel = torch.empty((n_masks, n_rows, sel_stride), dtype=torch.int32, device=mask_list.device)
+        cnt = torch.empty((n_masks, n_rows), dtype=torch.int32, device=mask_list.device)
+    else:
+        sel, cnt = out
+    check(lib().hp_selected_indices(_ptr(mask_list), _ptr(mask_count), cap, n_masks, n_rows,
+                                    block_size, query_offset, sink, stream_tokens, _ptr(sel),
+                                    _ptr(cnt), sel.shape[-1], C.c_void_p(_stream(stream))))
+    return sel, cnt
+
+
+def bsa(q: torch.Tensor, kv: PagedKV, sel: torch.Tensor, sel_count: torch.Tensor, *,
+        query_offset: int, max_sel: int, policy: RopePolicy | None = None,
+        rope: RopeTable | None = None, out: torch.Tensor | None = None,
+        partials=None, ws: Workspace | None = None, stream=None) -> torch.Tensor:
+    """Split-K block-sparse attention over selected lists; q fp32 [n_q_heads, n_rows, d]."""
+    policy = policy or RopePolicy()
+    ws = ws or Workspace(q.device)
+    hq, n_rows, d = q.shape
+    n_masks = sel.shape[0]
+    out = out if out is not None else torch.empty_like(q)
+    need = lib().hp_bsa_workspace_bytes(hq, n_rows, max_sel, d)
+    w = ws.get(need)
+    pm, pl, po = partials if partials is not None else (None, None, None)
+    a = BsaArgs(n_q_heads=hq, heads_per_mask=hq // n_masks, n_rows=n_rows, q=_ptr(q),
+                query_offset=query_offset, sel_list=_ptr(sel), sel_count=_ptr(sel_count),
+                sel_stride=sel.shape[-1], max_sel=max_sel, out=_ptr(out), part_m=_ptr(pm),
+                part_l=_ptr(pl), part_o=_ptr(po), workspace=_ptr(w), workspace_bytes=w.numel(),
+                kv=kv.view(), rope=policy.ctx(0, rope))
+    check(lib().hp_bsa(C.byref(a), C.c_void_p(_stream(stream))))
+    return out
+
+
+def lse_merge(m: torch.Tensor, l: torch.Tensor, o: torch.Tensor, out: torch.Tensor | None = None,
+              stream=None) -> torch.Tensor:
+    """Merge per-shard (m, l, o) triples: m, l [S, n]; o [S, n, d] -> [n, d]."""
+    s, n, d = o.shape
+    out = out if out is not None else torch.empty((n, d), dtype=torch.float32, device=o.device)
+    check(lib().hp_lse_merge(_ptr(m), _ptr(l), _ptr(o), s, n, d, _ptr(out), C.c_void_p(_stream(stream))))
+    return out
+
+
+# ------------------------------------------------------------------- decode layer
+class DecodeLayer:
+    """The per-layer decode body of DecodeEngine::step (decode.cpp:225-273) for one
+    token at position T-1: due stages chained through per-stage caches, then the
+    BSA over sinks ∪ last cache ∪ stream. Buffers are preallocated so the whole
+    step is CUDA-graph capturable.
+
+    q: fp32 [n_q_heads, d]; n_masks independent pooled masks (KV groups).
+    """
+
+    def __init__(self, kv: PagedKV, stages, *, sink: int, stream_tokens: int, n_q_heads: int,
+                 n_masks: int, layer1: int = 4, policy: RopePolicy | None = None,
+                 rope: RopeTable | None = None, device="cuda"):
+        require_cuda()
+        self.kv, self.stages = kv, [tuple(s) for s in stages]
+        self.sink, self.stream_tokens = sink, stream_tokens
+        self.n_q_heads, self.n_masks = n_q_heads, n_masks
+        self.layer1 = layer1
+        self.policy = policy or RopePolicy()
+        self.rope = rope
+        self.dev = torch.device(device)
+        self.ws = Workspace(self.dev)
+        self.caches = [(torch.zeros((n_masks, 1, s[2]), dtype=torch.int32, device=self.dev),
+                        torch.zeros((n_masks, 1), dtype=torch.int32, device=self.dev))
+                       for s in self.stages]
+        self.in_start = torch.full((n_masks, 1), sink, dtype=torch.int32, device=self.dev)
+        self.in_count = torch.zeros((n_masks, 1), dtype=torch.int32, device=self.dev)
+        keep_last = self.stages[-1][2]
+        self.sel_stride = sink + keep_last + stream_tokens + 1
+        self.sel = torch.zeros((n_masks, 1, self.sel_stride), dtype=torch.int32, device=self.dev)
+        self.sel_count = torch.zeros((n_masks, 1), dtype=torch.int32, device=self.dev)
+        self.q = torch.zeros((n_q_heads, 1, kv.d), dtype=torch.float32, device=self.dev)
+        self.out = torch.zeros((n_q_heads, 1, kv.d), dtype=torch.float32, device=self.dev)
+        # size the workspace once for the largest stage / BSA
+        t_max = kv.num_pages * kv.page_size
+        need = 0
+        prev = max(0, t_max - stream_tokens - sink)
+        for (_, lc, keep) in self.stages:
+            need = max(need, lib().hp_stage_workspace_bytes(n_masks, max(1, ceil_div(prev, lc)), keep, lc))
+            prev = keep
+        need = max(need, lib().hp_bsa_workspace_bytes(n_q_heads, 1, self.sel_stride, kv.d))
+        self.ws.get(need)
+
+    def set_t(self, t: int) -> None:
+        """Stage-1 input [n_sink, T - n_stream) for a context of T tokens (decode.cpp:232-240)."""
+        upper = t - self.stream_tokens if t > self.stream_tokens else 0
+        self.in_count.fill_(max(0, upper - self.sink))
+
+    def run(self, t: int, refresh=None, stream=None) -> torch.Tensor:
+        """One layer step at context length t (query position t-1). ``refresh`` flags which
+        stages are due (default: all). Reads self.q, writes self.out [n_q_heads, 1, d]."""
+        refresh = refresh if refresh is not None else [True] * len(self.stages)
+        pos = t - 1
+        upper = t - self.stream_tokens if t > self.stream_tokens else 0
+        n0 = max(0, upper - self.sink)
+        self.in_count.fill_(n0)
+        for i, ((bq, lc, keep), (cl, cc)) in enumerate(zip(self.stages, self.caches)):
+            if not refresh[i]:
+                continue
+            if i == 0:
+                kw = dict(in_start=self.in_start, in_count=self.in_count, max_chunks=ceil_div(n0, lc))
+            else:
+                pl, pc = self.caches[i - 1]
+                kw = dict(in_list=pl, in_count=pc, in_stride=pl.shape[-1],
+                          max_chunks=ceil_div(self.stages[i - 1][2], lc))
+            prune_stage((1, lc, keep), self.q, self.kv, n_masks=self.n_masks, n_blocks=1,
+                        out_list=cl, out_count=cc, query_offset=pos, stream_tokens=self.stream_tokens,
+                        layer1=self.layer1, policy=self.policy, rope=self.rope, ws=self.ws,
+                        stream=stream, **kw)
+        last_l, last_c = self.caches[-1]
+        selected_indices(last_l, last_c, n_rows=1, block_size=1, query_offset=pos, sink=self.sink,
+                         stream_tokens=self.stream_tokens, out=(self.sel, self.sel_count),
+                         stream=stream)
+        bsa(self.q, self.kv, self.sel, self.sel_count, query_offset=pos, max_sel=self.sel_stride,
+            policy=self.policy, rope=self.rope, out=self.out, ws=self.ws, stream=stream)
+        return self.out
