@@ -171,6 +171,78 @@ typedef struct hp_bsa_args {
 size_t hp_bsa_workspace_bytes(int32_t n_q_heads, int32_t n_rows, int32_t max_sel, int32_t d);
 int hp_bsa(const hp_bsa_args* args, void* stream);
 
+/* ------------------------------------------------------------------------ *
+ * Fused decode path (one query row per q-head, d = 128): the per-layer body of
+ * DecodeEngine::step (decode.cpp:225-273) as 1 kernel per stage + 1 BSA kernel.
+ * Stage outputs stay implicit between kernels: a stage emits only its kept
+ * chunk ids (sel) and the next stage resolves list positions through them
+ * (hp_list_ref); hp_decode_materialize expands any stage's list on demand
+ * (the DecodeEngine stage caches, decode.hpp:85-90).
+ * ------------------------------------------------------------------------ */
+typedef struct hp_list_ref {
+    int32_t depth;               /* number of chunk-selection hops (<= 4)               */
+    int32_t pad_;
+    const int32_t* sel[4];       /* hop i: kept chunk ids [n_masks][sel_stride[i]]       */
+    int32_t sel_stride[4];
+    int32_t lc[4];               /* chunk size of hop i                                 */
+    const int32_t* base_list;    /* NULL => base is the range [range_start, ...)        */
+    int64_t base_stride;
+    int64_t range_start;
+} hp_list_ref;
+
+typedef struct hp_decode_stage_args {
+    int32_t chunk_size;
+    int32_t keep;
+    int32_t n_masks;
+    int32_t heads_per_mask;
+    int32_t n_q_heads;
+    int32_t stream_tokens;
+    const float* q;              /* [n_q_heads][d] fp32                                 */
+    int64_t query_position;      /* T - 1                                               */
+    hp_list_ref in;              /* input list per mask                                 */
+    const int32_t* in_count;     /* [n_masks] device counts, or NULL => in_count_const  */
+    int64_t in_count_const;
+    int32_t max_chunks;          /* >= ceil(in_count / chunk_size)                      */
+    int32_t sel_stride;          /* >= keep / chunk_size                                */
+    int32_t* sel_out;            /* [n_masks][sel_stride] kept chunk ids, ascending     */
+    int32_t* out_count;          /* [n_masks] output list length                        */
+    void* workspace;             /* >= hp_decode_stage_workspace_bytes()                */
+    size_t workspace_bytes;
+    hp_kv_view keys;
+    hp_rope_ctx rope;
+} hp_decode_stage_args;
+
+size_t hp_decode_stage_workspace_bytes(int32_t n_masks, int32_t max_chunks);
+int hp_decode_stage(const hp_decode_stage_args* args, void* stream);
+
+typedef struct hp_decode_bsa_args {
+    int32_t n_q_heads;
+    int32_t heads_per_mask;
+    int32_t sink_tokens;
+    int32_t stream_tokens;
+    const float* q;              /* [n_q_heads][d] fp32                                 */
+    int64_t query_position;
+    hp_list_ref mask;            /* middle indices per mask (all in [sink_end, stream_begin)) */
+    const int32_t* mask_count;   /* [n_masks] */
+    int32_t max_mask;            /* upper bound on mask counts                          */
+    float* out;                  /* [n_q_heads][d] fp32                                 */
+    float* part_m;               /* optional shard LSE triple (m, l [n_q_heads], o [n_q_heads][d]) */
+    float* part_l;
+    float* part_o;
+    void* workspace;
+    size_t workspace_bytes;
+    hp_kv_view kv;
+    hp_rope_ctx rope;
+} hp_decode_bsa_args;
+
+size_t hp_decode_bsa_workspace_bytes(int32_t n_q_heads, int32_t max_sel);
+int hp_decode_bsa(const hp_decode_bsa_args* args, void* stream);
+
+/* Expand lists: out[m][i] = ref(m, i) for i < count[m] (n_lists refs at once). */
+int hp_decode_materialize(const hp_list_ref* refs, const int32_t* const* counts,
+                          int32_t* const* outs, const int64_t* out_strides, int32_t n_lists,
+                          int32_t n_masks, int32_t max_count, void* stream);
+
 /* Log-sum-exp merge of per-shard (m, l, o) partials (C5 sequence sharding):
  * m, l [n_shards][n]; o [n_shards][n][d] -> out [n][d]. */
 int hp_lse_merge(const float* m, const float* l, const float* o, int32_t n_shards, int32_t n,

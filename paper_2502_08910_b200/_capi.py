@@ -68,12 +68,39 @@ class BsaArgs(C.Structure):
                 ("workspace_bytes", C.c_size_t), ("kv", KvView), ("rope", RopeCtx)]
 
 
+class ListRef(C.Structure):
+    _fields_ = [("depth", C.c_int32), ("pad_", C.c_int32), ("sel", C.c_void_p * 4),
+                ("sel_stride", C.c_int32 * 4), ("lc", C.c_int32 * 4), ("base_list", C.c_void_p),
+                ("base_stride", C.c_int64), ("range_start", C.c_int64)]
+
+
+class DecodeStageArgs(C.Structure):
+    _fields_ = [("chunk_size", C.c_int32), ("keep", C.c_int32), ("n_masks", C.c_int32),
+                ("heads_per_mask", C.c_int32), ("n_q_heads", C.c_int32),
+                ("stream_tokens", C.c_int32), ("q", C.c_void_p), ("query_position", C.c_int64),
+                ("in_", ListRef), ("in_count", C.c_void_p), ("in_count_const", C.c_int64),
+                ("max_chunks", C.c_int32), ("sel_stride", C.c_int32), ("sel_out", C.c_void_p),
+                ("out_count", C.c_void_p), ("workspace", C.c_void_p),
+                ("workspace_bytes", C.c_size_t), ("keys", KvView), ("rope", RopeCtx)]
+
+
+class DecodeBsaArgs(C.Structure):
+    _fields_ = [("n_q_heads", C.c_int32), ("heads_per_mask", C.c_int32),
+                ("sink_tokens", C.c_int32), ("stream_tokens", C.c_int32), ("q", C.c_void_p),
+                ("query_position", C.c_int64), ("mask", ListRef), ("mask_count", C.c_void_p),
+                ("max_mask", C.c_int32), ("out", C.c_void_p), ("part_m", C.c_void_p),
+                ("part_l", C.c_void_p), ("part_o", C.c_void_p), ("workspace", C.c_void_p),
+                ("workspace_bytes", C.c_size_t), ("kv", KvView), ("rope", RopeCtx)]
+
+
 _lib = None
 
 # every symbol include/hipprune_b200.h declares
 EXPORTS = ["hp_last_error", "hp_version", "hp_device_available", "hp_build_rope_table",
            "hp_stage_workspace_bytes", "hp_prune_stage", "hp_remap_blocks",
-           "hp_selected_indices", "hp_bsa_workspace_bytes", "hp_bsa", "hp_lse_merge"]
+           "hp_selected_indices", "hp_bsa_workspace_bytes", "hp_bsa", "hp_lse_merge",
+           "hp_decode_stage_workspace_bytes", "hp_decode_stage", "hp_decode_bsa_workspace_bytes",
+           "hp_decode_bsa", "hp_decode_materialize"]
 
 
 def lib():
@@ -106,6 +133,18 @@ def lib():
     L.hp_bsa_workspace_bytes.argtypes = [C.c_int32] * 4
     L.hp_bsa.restype = C.c_int
     L.hp_bsa.argtypes = [C.POINTER(BsaArgs), C.c_void_p]
+    L.hp_decode_stage_workspace_bytes.restype = C.c_size_t
+    L.hp_decode_stage_workspace_bytes.argtypes = [C.c_int32, C.c_int32]
+    L.hp_decode_stage.restype = C.c_int
+    L.hp_decode_stage.argtypes = [C.POINTER(DecodeStageArgs), C.c_void_p]
+    L.hp_decode_bsa_workspace_bytes.restype = C.c_size_t
+    L.hp_decode_bsa_workspace_bytes.argtypes = [C.c_int32, C.c_int32]
+    L.hp_decode_bsa.restype = C.c_int
+    L.hp_decode_bsa.argtypes = [C.POINTER(DecodeBsaArgs), C.c_void_p]
+    L.hp_decode_materialize.restype = C.c_int
+    L.hp_decode_materialize.argtypes = [C.POINTER(ListRef), C.POINTER(C.c_void_p),
+                                        C.POINTER(C.c_void_p), C.POINTER(C.c_int64), C.c_int32,
+                                        C.c_int32, C.c_int32, C.c_void_p]
     L.hp_lse_merge.restype = C.c_int
     L.hp_lse_merge.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
                                C.c_int32, C.c_void_p, C.c_void_p]

@@ -18,7 +18,7 @@ LIB = PKG / "_lib"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",
               f"-I{ROOT / 'include'}", f"-I{CSRC}"]
-CUDA_SOURCES = ["prune.cu", "bsa.cu", "capi.cu"]
+CUDA_SOURCES = ["prune.cu", "bsa.cu", "decode.cu", "capi.cu"]
 
 
 def nvcc() -> str:
@@ -38,7 +38,7 @@ def _stale(target: Path, deps) -> bool:
 def build_cuda(force: bool = False, verbose: bool = False) -> Path:
     LIB.mkdir(exist_ok=True)
     out = LIB / "libhipprune_b200.so"
-    deps = [CSRC / s for s in CUDA_SOURCES] + list(CSRC.glob("*.cuh")) + [ROOT / "include" / "hipprune_b200.h"]
+    deps = [CSRC / s for s in CUDA_SOURCES] + list(CSRC.glob("*.cuh")) + [ROOT / "include" / "hipprune_b200.h", Path(__file__)]
     if not force and not _stale(out, deps):
         return out
     objs = []

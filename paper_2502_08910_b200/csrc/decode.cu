@@ -1,0 +1,729 @@
+// Fused decode path (d = 128): one kernel per pruning stage with the exact
+// top-k fused into the last CTA of each mask, implicit stage lists, and a
+// segment-mode split-K BSA with a fused log-sum-exp combine.
+//
+// Reference semantics (paths relative to /root/reference/proj):
+//   stage descent / scores / top-k   pruning.cpp:69-98,153-200, tensor.cpp:88-114
+//   decode stage chaining            decode.cpp:225-249 (stage i consumes stage i-1)
+//   selected set for the token       sparse_attention.cpp:95-112 (1-row block)
+//   attention_row                    sparse_attention.cpp:33-60
+// Exactness contract as in prune.cu: sequential separately-rounded fp32 dots,
+// Alg. 3 descent with strict '>', stable (score desc, chunk asc) top-k.
+//
+// B200 mapping. Stage 1 at 1M ctx x 8 KV groups is 131K independent descents of
+// 9 dependent 256 B row gathers; it is HBM-bound only if all of them are in
+// flight at once. A warp owns 32 descents (lane = chunk) of one q-head and
+// stages its 32 rows per step in 8 KB of shared memory with 16 B cp.async
+// (XOR-swizzled 16 B chunks: conflict-free LDS.128 without padding), so 7 CTAs
+// of 4 warps (<= 72 registers/thread) fit per SM and the whole stage is one
+// wave. The mask's last CTA to finish (atomic ticket) runs the radix select on
+// the mask's chunk scores and emits only the kept chunk ids; the next stage
+// resolves its input positions through them (hp_list_ref), so the 32K / 8K
+// intermediate index lists never touch HBM on the critical path.
+
+#include <algorithm>
+#include <cmath>
+
+#include "common.cuh"
+
+using namespace hpk;
+
+namespace {
+
+constexpr int kD = 128;
+constexpr int kStageWarps = 4;     // warps per stage CTA
+constexpr int kBsaWarps = 8;
+constexpr int kBsaKeysPerWarp = 8;
+constexpr int kBsaKeysPerCta = kBsaWarps * kBsaKeysPerWarp;  // 64
+constexpr int kMaxHC = 8;
+
+__device__ __forceinline__ int64_t ref_token(const hp_list_ref& L, int mask, int64_t pos) {
+#pragma unroll 1
+    for (int i = L.depth - 1; i >= 0; --i) {
+        const int64_t lc = L.lc[i];
+        const int64_t r = pos / lc;
+        pos = static_cast<int64_t>(L.sel[i][static_cast<int64_t>(mask) * L.sel_stride[i] + r]) * lc + (pos - r * lc);
+    }
+    return L.base_list ? static_cast<int64_t>(L.base_list[mask * L.base_stride + pos]) : L.range_start + pos;
+}
+
+// ----------------------------------------------------------------------------- dots
+// Sequential fp32 dot of q (shared, broadcast) with the lane's staged row.
+template <typename T>
+__device__ __forceinline__ float dot_row(const unsigned char* row, int swz, const float* q);
+
+template <>
+__device__ __forceinline__ float dot_row<bf16_t>(const unsigned char* row, int swz, const float* q) {
+    const float4* q4 = reinterpret_cast<const float4*>(q);
+    float acc = 0.0f;
+#pragma unroll 4
+    for (int c = 0; c < 16; ++c) {
+        const uint4 w = *reinterpret_cast<const uint4*>(row + ((c ^ swz) << 4));
+        const float4 qa = q4[2 * c], qb = q4[2 * c + 1];
+        acc = __fadd_rn(acc, __fmul_rn(qa.x, bf16_lo(w.x)));
+        acc = __fadd_rn(acc, __fmul_rn(qa.y, bf16_hi(w.x)));
+        acc = __fadd_rn(acc, __fmul_rn(qa.z, bf16_lo(w.y)));
+        acc = __fadd_rn(acc, __fmul_rn(qa.w, bf16_hi(w.y)));
+        acc = __fadd_rn(acc, __fmul_rn(qb.x, bf16_lo(w.z)));
+        acc = __fadd_rn(acc, __fmul_rn(qb.y, bf16_hi(w.z)));
+        acc = __fadd_rn(acc, __fmul_rn(qb.z, bf16_lo(w.w)));
+        acc = __fadd_rn(acc, __fmul_rn(qb.w, bf16_hi(w.w)));
+    }
+    return acc;
+}
+
+template <>
+__device__ __forceinline__ float dot_row<float>(const unsigned char* row, int swz, const float* q) {
+    const float4* q4 = reinterpret_cast<const float4*>(q);
+    float acc = 0.0f;
+#pragma unroll 4
+    for (int c = 0; c < 32; ++c) {
+        const float4 w = *reinterpret_cast<const float4*>(row + ((c ^ swz) << 4));
+        const float4 qa = q4[c];
+        acc = __fadd_rn(acc, __fmul_rn(qa.x, w.x));
+        acc = __fadd_rn(acc, __fmul_rn(qa.y, w.y));
+        acc = __fadd_rn(acc, __fmul_rn(qa.z, w.z));
+        acc = __fadd_rn(acc, __fmul_rn(qa.w, w.w));
+    }
+    return acc;
+}
+
+template <typename T>
+__device__ __forceinline__ float elem(const unsigned char* row, int swz, int i) {
+    constexpr int per = 16 / sizeof(T);
+    const int c = i / per, o = i - c * per;
+    const T* p = reinterpret_cast<const T*>(row + ((c ^ swz) << 4));
+    return load_elem(p, o);
+}
+
+// Rotated dot: apply_rope_inplace (tensor.cpp:61-79) then the sequential dot.
+template <typename T>
+__device__ __forceinline__ float dot_row_rot(const unsigned char* row, int swz, const float* q,
+                                             const float* cs, const float* sn) {
+    float acc = 0.0f;
+    constexpr int half = kD / 2;
+#pragma unroll 2
+    for (int i = 0; i < half; ++i) {
+        const float x = elem<T>(row, swz, i), y = elem<T>(row, swz, i + half);
+        const float r = __fsub_rn(__fmul_rn(x, __ldg(cs + i)), __fmul_rn(y, __ldg(sn + i)));
+        acc = __fadd_rn(acc, __fmul_rn(q[i], r));
+    }
+#pragma unroll 2
+    for (int i = 0; i < half; ++i) {
+        const float x = elem<T>(row, swz, i), y = elem<T>(row, swz, i + half);
+        const float r = __fadd_rn(__fmul_rn(x, __ldg(sn + i)), __fmul_rn(y, __ldg(cs + i)));
+        acc = __fadd_rn(acc, __fmul_rn(q[half + i], r));
+    }
+    return acc;
+}
+
+// ------------------------------------------------------------------------ staging
+template <typename T>
+struct RowGeom {
+    static constexpr int bytes = kD * sizeof(T);        // 256 or 512
+    static constexpr int chunks = bytes / 16;           // 16 or 32
+    static constexpr int rows_per_instr = 32 / chunks;  // 2 or 1
+};
+
+// Gather one key row per active lane into the warp's swizzled staging area.
+template <typename T>
+__device__ __forceinline__ void stage_rows(const hp_kv_view& kv, int kvh, int64_t tok,
+                                           unsigned char* ks, int lane) {
+    using G = RowGeom<T>;
+    const char* p = tok >= 0 ? kv_row_ptr(kv, kv.k_pool, kv.k_host, kvh, tok, sizeof(T)) : nullptr;
+    const unsigned long long pu = reinterpret_cast<unsigned long long>(p);
+    const int c = lane % G::chunks, sub = lane / G::chunks;
+#pragma unroll
+    for (int r = 0; r < 32; r += G::rows_per_instr) {
+        const int row = r + sub;
+        const unsigned long long pp = __shfl_sync(0xffffffffu, pu, row);
+        if (pp) cp_async16(ks + row * G::bytes + ((c ^ (row & (G::chunks - 1))) << 4),
+                           reinterpret_cast<const char*>(pp) + (c << 4));
+    }
+    cp_async_wait_all();
+    __syncwarp();
+}
+
+// ----------------------------------------------------------------------- top-k
+// Exclusive scan over the CTA for any multiple-of-32 block size.
+__device__ __forceinline__ int block_scan_rt(int v, int* tmp) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) tmp[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        int t = lane < nw ? tmp[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += y;
+        }
+        if (lane < nw) tmp[lane] = t;
+    }
+    __syncthreads();
+    const int base = w ? tmp[w - 1] : 0;
+    __syncthreads();
+    return base + x - v;
+}
+
+// Exact top-K of `cc` chunk scores for one mask by the whole CTA: radix select
+// on order keys (-0 folded onto +0), ties to the lowest chunk index, survivors
+// emitted in ascending chunk order (pruning.cpp:187-192).
+__device__ void cta_topk(const float* sc, int64_t cc, int K, int32_t* sel_out, uint32_t* skeys,
+                         int smem_cap) {
+    __shared__ int hist[256];
+    __shared__ int scan_tmp[32];
+    __shared__ int sh_digit, sh_above;
+    const int nt = blockDim.x;
+    const bool in_smem = cc <= smem_cap;
+    if (in_smem) {
+        for (int64_t j = threadIdx.x; j < cc; j += nt) skeys[j] = order_key(__ldcg(sc + j));
+        __syncthreads();
+    }
+    auto key = [&](int64_t j) -> uint32_t { return in_smem ? skeys[j] : order_key(__ldcg(sc + j)); };
+    uint32_t prefix = 0, pmask = 0;
+    int need = K;
+    for (int shift = 24; shift >= 0; shift -= 8) {
+        for (int i = threadIdx.x; i < 256; i += nt) hist[i] = 0;
+        __syncthreads();
+        for (int64_t j = threadIdx.x; j < cc; j += nt) {
+            const uint32_t u = key(j);
+            if ((u & pmask) == prefix) atomicAdd(&hist[(u >> shift) & 255u], 1);
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            const int lane = threadIdx.x;
+            int c[8], tot = 0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) { c[k] = hist[lane * 8 + k]; tot += c[k]; }
+            int suf = tot;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_down_sync(0xffffffffu, suf, o);
+                if (lane + o < 32) suf += y;
+            }
+            int above = suf - tot;
+#pragma unroll
+            for (int k = 7; k >= 0; --k) {
+                if (above < need && need <= above + c[k]) { sh_digit = lane * 8 + k; sh_above = above; }
+                above += c[k];
+            }
+        }
+        __syncthreads();
+        prefix |= static_cast<uint32_t>(sh_digit) << shift;
+        pmask |= 255u << shift;
+        need -= sh_above;
+        __syncthreads();
+    }
+    // Each thread owns a contiguous run of chunk indices so ranks follow index order.
+    const int64_t per = (cc + nt - 1) / nt;
+    const int64_t j0 = min64(cc, threadIdx.x * per), j1 = min64(cc, j0 + per);
+    int ties = 0, gts = 0;
+    for (int64_t j = j0; j < j1; ++j) {
+        const uint32_t u = key(j);
+        ties += u == prefix;
+        gts += u > prefix;
+    }
+    const int tie_base = block_scan_rt(ties, scan_tmp);
+    const int take = gts + max(0, min(need - tie_base, ties));
+    int r = block_scan_rt(take, scan_tmp);
+    int trank = tie_base;
+    for (int64_t j = j0; j < j1; ++j) {
+        const uint32_t u = key(j);
+        bool s = u > prefix;
+        if (u == prefix) { s = trank < need; ++trank; }
+        if (s) sel_out[r++] = static_cast<int32_t>(j);
+    }
+    __syncthreads();
+}
+
+// ------------------------------------------------------------------ stage kernel
+template <typename T, bool EXT>
+__global__ void __launch_bounds__(kStageWarps * 32, 7)
+decode_stage_kernel(const hp_decode_stage_args a, float* scores, int* tickets, int cg) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    using G = RowGeom<T>;
+    const int hpm = a.heads_per_mask;
+    const int m = blockIdx.y;
+    const int64_t n_in = a.in_count ? a.in_count[m] : a.in_count_const;
+    const int lc = a.chunk_size;
+    const int64_t cc = (n_in + lc - 1) / lc;
+    const int K = a.keep / lc;
+    const int chunks_per_cta = 32 * cg;
+    const int64_t chunk0 = static_cast<int64_t>(blockIdx.x) * chunks_per_cta;
+
+    if (n_in <= a.keep || cc <= K) {  // identity (pruning.cpp:159-168): keep every chunk
+        if (blockIdx.x == 0) {
+            for (int64_t j = threadIdx.x; j < cc; j += blockDim.x) a.sel_out[static_cast<int64_t>(m) * a.sel_stride + j] = static_cast<int32_t>(j);
+            if (threadIdx.x == 0) a.out_count[m] = static_cast<int32_t>(n_in);
+        }
+        return;
+    }
+    if (chunk0 >= cc) return;
+
+    const int nwarps = blockDim.x >> 5;
+    float* qs = reinterpret_cast<float*>(smem);                       // [hpm][128]
+    float* red = qs + hpm * kD;                                       // [hpm][chunks_per_cta]
+    unsigned char* stage = reinterpret_cast<unsigned char*>(red + hpm * chunks_per_cta);
+    stage = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(stage) + 127) & ~uintptr_t(127));
+
+    for (int i = threadIdx.x; i < hpm * kD; i += blockDim.x) qs[i] = a.q[static_cast<int64_t>(m * hpm) * kD + i];
+    __syncthreads();
+    if constexpr (EXT) {
+        constexpr int half = kD / 2;
+        const int64_t qp = rope_q_position(a.rope, a.query_position, a.stream_tokens, cc);
+        for (int i = threadIdx.x; i < hpm * half; i += blockDim.x) {
+            const int hh = i / half, e = i - hh * half;
+            float* row = qs + hh * kD;
+            const float c = a.rope.cos_tab[qp * half + e], s = a.rope.sin_tab[qp * half + e];
+            const float x = row[e], y = row[e + half];
+            row[e] = __fsub_rn(__fmul_rn(x, c), __fmul_rn(y, s));
+            row[e + half] = __fadd_rn(__fmul_rn(x, s), __fmul_rn(y, c));
+        }
+        __syncthreads();
+    }
+
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    unsigned char* ks = stage + static_cast<size_t>(w) * 32 * G::bytes;
+    const unsigned char* myrow = ks + lane * G::bytes;
+    const int swz = lane & (G::chunks - 1);
+
+    for (int item = w; item < hpm * cg; item += nwarps) {
+        const int hh = item % hpm, grp = item / hpm;
+        const int qh = m * hpm + hh;
+        const int kvh = qh / (a.n_q_heads / a.keys.n_kv);
+        const float* qrow = qs + hh * kD;
+        const int64_t j = chunk0 + grp * 32 + lane;
+        const bool active = j < cc;
+        const int64_t base = j * lc;
+        const int len = active ? static_cast<int>(min64(lc, n_in - base)) : 0;
+        int64_t t_first = 0;
+        bool contiguous = true;
+        if (active) {
+            t_first = ref_token(a.in, m, base);
+            if (len > 1) contiguous = ref_token(a.in, m, base + len - 1) - t_first == len - 1;
+        }
+        auto token = [&](int i) -> int64_t { return contiguous ? t_first + i : ref_token(a.in, m, base + i); };
+        const float* cs1 = nullptr; const float* sn1 = nullptr;
+        const float* cs2 = nullptr; const float* sn2 = nullptr;
+        bool same_rot = true;
+        if constexpr (EXT) {
+            constexpr int half = kD / 2;
+            const int64_t p1 = rope_k_position(a.rope, 1, j), p2 = rope_k_position(a.rope, 2, j);
+            cs1 = a.rope.cos_tab + p1 * half; sn1 = a.rope.sin_tab + p1 * half;
+            cs2 = a.rope.cos_tab + p2 * half; sn2 = a.rope.sin_tab + p2 * half;
+            same_rot = p1 == p2;
+        }
+        int first = 1, last = len, it = 0, iters = 0;
+        while ((1 << iters) < len) ++iters;
+        float s1 = 0.f, s2 = 0.f;
+        stage_rows<T>(a.keys, kvh, active ? token(0) : -1, ks, lane);
+        if (active) {
+            if constexpr (EXT) {
+                s1 = dot_row_rot<T>(myrow, swz, qrow, cs1, sn1);
+                s2 = same_rot ? s1 : dot_row_rot<T>(myrow, swz, qrow, cs2, sn2);
+            } else {
+                s1 = s2 = dot_row<T>(myrow, swz, qrow);
+            }
+        }
+        for (;;) {
+            const bool go = active && it < iters && first < last;
+            if (!__any_sync(0xffffffffu, go)) break;
+            const int mid = (first + last + 1) >> 1;
+            __syncwarp();
+            stage_rows<T>(a.keys, kvh, go ? token(mid - 1) : -1, ks, lane);
+            if (go) {
+                float m1, m2;
+                if constexpr (EXT) {
+                    m1 = dot_row_rot<T>(myrow, swz, qrow, cs1, sn1);
+                    m2 = same_rot ? m1 : dot_row_rot<T>(myrow, swz, qrow, cs2, sn2);
+                } else {
+                    m1 = m2 = dot_row<T>(myrow, swz, qrow);
+                }
+                if (m2 > s1) { first = mid; s1 = m1; s2 = m2; } else { last = mid - 1; }
+                ++it;
+            }
+        }
+        red[hh * chunks_per_cta + grp * 32 + lane] = s2;
+        __syncwarp();
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < chunks_per_cta; c += blockDim.x) {
+        const int64_t jj = chunk0 + c;
+        if (jj >= cc) continue;
+        float best = -INFINITY;
+        for (int h = 0; h < hpm; ++h) {
+            const float s = red[h * chunks_per_cta + c];
+            best = (best < s) ? s : best;  // std::max (pruning.cpp:182)
+        }
+        scores[static_cast<int64_t>(m) * a.max_chunks + jj] = best;
+    }
+    // last CTA of this mask runs the selection
+    __shared__ int sh_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int total = static_cast<int>((cc + chunks_per_cta - 1) / chunks_per_cta);
+        const int prev = atomicAdd(&tickets[m], 1);
+        sh_last = prev == total - 1;
+        if (sh_last) tickets[m] = 0;  // self-reset for the next launch / graph replay
+    }
+    __syncthreads();
+    if (!sh_last) return;
+    __threadfence();
+    const int smem_cap = static_cast<int>((static_cast<size_t>(nwarps) * 32 * G::bytes) / 4);
+    int32_t* sel = a.sel_out + static_cast<int64_t>(m) * a.sel_stride;
+    cta_topk(scores + static_cast<int64_t>(m) * a.max_chunks, cc, K, sel,
+             reinterpret_cast<uint32_t*>(stage), smem_cap);
+    if (threadIdx.x == 0) {
+        const int64_t lastc = sel[K - 1];
+        a.out_count[m] = static_cast<int32_t>(static_cast<int64_t>(K - 1) * lc + min64(lc, n_in - lastc * lc));
+    }
+}
+
+// -------------------------------------------------------------------- BSA kernel
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+template <typename T> struct Pair;
+template <> struct Pair<bf16_t> {
+    using V = uint32_t;
+    static __device__ __forceinline__ V ld(const void* p) { return __ldg(reinterpret_cast<const unsigned int*>(p)); }
+    static __device__ __forceinline__ float lo(V v) { return bf16_lo(v); }
+    static __device__ __forceinline__ float hi(V v) { return bf16_hi(v); }
+};
+template <> struct Pair<float> {
+    using V = float2;
+    static __device__ __forceinline__ V ld(const void* p) { return __ldg(reinterpret_cast<const float2*>(p)); }
+    static __device__ __forceinline__ float lo(V v) { return v.x; }
+    static __device__ __forceinline__ float hi(V v) { return v.y; }
+};
+
+// grid = (splits, n_q_heads / HC); CTA covers 64 consecutive selected positions for
+// HC q-heads sharing one kv head and one mask. Lane L holds elements 2L, 2L+1 and
+// their RoPE partners 64+2L, 65+2L. The last CTA of each head group merges.
+template <typename T, int HC, bool EXT>
+__global__ void __launch_bounds__(kBsaWarps * 32, 2)
+decode_bsa_kernel(const hp_decode_bsa_args a, float* part, int* tickets, int splits) {
+    using P = Pair<T>;
+    __shared__ float sm_m[kBsaWarps][HC], sm_l[kBsaWarps][HC];
+    __shared__ float sm_o[kBsaWarps][HC][kD];
+    __shared__ int sh_last;
+    const int split = blockIdx.x, hg = blockIdx.y;
+    const int h0 = hg * HC;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int mask = h0 / a.heads_per_mask;
+    const int kvh = h0 / (a.n_q_heads / a.kv.n_kv);
+    const int64_t pos = a.query_position;
+    const int64_t sink_end = min64(a.sink_tokens, pos + 1);
+    int64_t stream_begin = pos + 1 > a.stream_tokens ? pos + 1 - a.stream_tokens : 0;
+    stream_begin = max64(stream_begin, sink_end);
+    const int64_t n_mask = a.mask_count[mask];
+    const int64_t n_sel = sink_end + n_mask + (pos + 1 - stream_begin);
+    const float scale = 1.0f / sqrtf(static_cast<float>(kD));
+    constexpr int half = kD / 2;
+
+    float qx[HC][2], qy[HC][2];
+#pragma unroll
+    for (int hh = 0; hh < HC; ++hh) {
+        const float* qr = a.q + static_cast<int64_t>(h0 + hh) * kD;
+        float x0 = qr[2 * lane], x1 = qr[2 * lane + 1], y0 = qr[half + 2 * lane], y1 = qr[half + 2 * lane + 1];
+        if constexpr (EXT) {
+            const float* c = a.rope.cos_tab + pos * half;
+            const float* s = a.rope.sin_tab + pos * half;
+            const float c0 = c[2 * lane], c1 = c[2 * lane + 1], s0 = s[2 * lane], s1 = s[2 * lane + 1];
+            const float nx0 = x0 * c0 - y0 * s0, ny0 = x0 * s0 + y0 * c0;
+            const float nx1 = x1 * c1 - y1 * s1, ny1 = x1 * s1 + y1 * c1;
+            x0 = nx0; y0 = ny0; x1 = nx1; y1 = ny1;
+        }
+        qx[hh][0] = x0; qx[hh][1] = x1; qy[hh][0] = y0; qy[hh][1] = y1;
+    }
+
+    // this warp's 8 positions
+    const int64_t p0 = static_cast<int64_t>(split) * kBsaKeysPerCta + w * kBsaKeysPerWarp;
+    int64_t tok_l = -1;
+    if (lane < kBsaKeysPerWarp) {
+        const int64_t p = p0 + lane;
+        if (p < n_sel) {
+            if (p < sink_end) tok_l = p;
+            else if (p < sink_end + n_mask) tok_l = ref_token(a.mask, mask, p - sink_end);
+            else tok_l = stream_begin + (p - sink_end - n_mask);
+        }
+    }
+    typename P::V kr[kBsaKeysPerWarp][2], vr[kBsaKeysPerWarp][2];
+    int64_t toks[kBsaKeysPerWarp];
+#pragma unroll
+    for (int k = 0; k < kBsaKeysPerWarp; ++k) {
+        toks[k] = __shfl_sync(0xffffffffu, tok_l, k);
+        if (toks[k] >= 0) {
+            const char* kp = kv_row_ptr(a.kv, a.kv.k_pool, a.kv.k_host, kvh, toks[k], sizeof(T));
+            const char* vp = kv_row_ptr(a.kv, a.kv.v_pool, a.kv.v_host, kvh, toks[k], sizeof(T));
+            kr[k][0] = P::ld(kp + 2 * lane * sizeof(T));
+            kr[k][1] = P::ld(kp + (half + 2 * lane) * sizeof(T));
+            vr[k][0] = P::ld(vp + 2 * lane * sizeof(T));
+            vr[k][1] = P::ld(vp + (half + 2 * lane) * sizeof(T));
+        } else {
+            kr[k][0] = kr[k][1] = vr[k][0] = vr[k][1] = typename P::V{};
+        }
+    }
+    float kx[kBsaKeysPerWarp][2], ky[kBsaKeysPerWarp][2];
+#pragma unroll
+    for (int k = 0; k < kBsaKeysPerWarp; ++k) {
+        float x0 = P::lo(kr[k][0]), x1 = P::hi(kr[k][0]), y0 = P::lo(kr[k][1]), y1 = P::hi(kr[k][1]);
+        if constexpr (EXT) {
+            if (toks[k] >= 0) {
+                const int64_t kp = pos + 1 - n_sel + (p0 + k);  // streaming_positions (rope_policy.cpp:59-72)
+                const float* c = a.rope.cos_tab + kp * half;
+                const float* s = a.rope.sin_tab + kp * half;
+                const float c0 = c[2 * lane], c1 = c[2 * lane + 1], s0 = s[2 * lane], s1 = s[2 * lane + 1];
+                const float nx0 = x0 * c0 - y0 * s0, ny0 = x0 * s0 + y0 * c0;
+                const float nx1 = x1 * c1 - y1 * s1, ny1 = x1 * s1 + y1 * c1;
+                x0 = nx0; y0 = ny0; x1 = nx1; y1 = ny1;
+            }
+        }
+        kx[k][0] = x0; kx[k][1] = x1; ky[k][0] = y0; ky[k][1] = y1;
+    }
+#pragma unroll
+    for (int hh = 0; hh < HC; ++hh) {
+        float s[kBsaKeysPerWarp];
+        float mt = -INFINITY;
+#pragma unroll
+        for (int k = 0; k < kBsaKeysPerWarp; ++k) {
+            float part_dot = qx[hh][0] * kx[k][0] + qx[hh][1] * kx[k][1] + qy[hh][0] * ky[k][0] + qy[hh][1] * ky[k][1];
+            part_dot = warp_sum(part_dot);
+            s[k] = toks[k] >= 0 ? part_dot * scale : -INFINITY;
+            mt = fmaxf(mt, s[k]);
+        }
+        float l = 0.f, o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f;
+        if (mt != -INFINITY) {
+#pragma unroll
+            for (int k = 0; k < kBsaKeysPerWarp; ++k) {
+                const float p = toks[k] >= 0 ? expf(s[k] - mt) : 0.f;
+                l += p;
+                o0 += p * P::lo(vr[k][0]); o1 += p * P::hi(vr[k][0]);
+                o2 += p * P::lo(vr[k][1]); o3 += p * P::hi(vr[k][1]);
+            }
+        }
+        if (lane == 0) { sm_m[w][hh] = mt; sm_l[w][hh] = l; }
+        sm_o[w][hh][2 * lane] = o0; sm_o[w][hh][2 * lane + 1] = o1;
+        sm_o[w][hh][half + 2 * lane] = o2; sm_o[w][hh][half + 2 * lane + 1] = o3;
+    }
+    __syncthreads();
+    // CTA partial per head -> workspace [hg][split][hh][2 + 128]
+    for (int idx = threadIdx.x; idx < HC * kD; idx += blockDim.x) {
+        const int hh = idx / kD, e = idx - hh * kD;
+        float M = -INFINITY;
+#pragma unroll
+        for (int ww = 0; ww < kBsaWarps; ++ww) M = fmaxf(M, sm_m[ww][hh]);
+        float L = 0.f, o = 0.f;
+        if (M != -INFINITY) {
+#pragma unroll
+            for (int ww = 0; ww < kBsaWarps; ++ww) {
+                const float f = sm_m[ww][hh] == -INFINITY ? 0.f : expf(sm_m[ww][hh] - M);
+                L += sm_l[ww][hh] * f;
+                o += sm_o[ww][hh][e] * f;
+            }
+        }
+        float* pp = part + ((static_cast<int64_t>(hg) * splits + split) * HC + hh) * (kD + 2);
+        if (e == 0) { pp[0] = M; pp[1] = L; }
+        pp[2 + e] = o;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int prev = atomicAdd(&tickets[hg], 1);
+        sh_last = prev == splits - 1;
+        if (sh_last) tickets[hg] = 0;
+    }
+    __syncthreads();
+    if (!sh_last) return;
+    __threadfence();
+    // merge all splits of this head group (log-sum-exp)
+    for (int idx = threadIdx.x; idx < HC * kD; idx += blockDim.x) {
+        const int hh = idx / kD, e = idx - hh * kD;
+        const float* pb = part + (static_cast<int64_t>(hg) * splits * HC + hh) * (kD + 2);
+        float M = -INFINITY;
+        for (int s = 0; s < splits; ++s) {
+            const float* pp = pb + static_cast<int64_t>(s) * HC * (kD + 2);
+            if (__ldcg(pp + 1) > 0.f) M = fmaxf(M, __ldcg(pp));
+        }
+        float L = 0.f, o = 0.f;
+        for (int s = 0; s < splits; ++s) {
+            const float* pp = pb + static_cast<int64_t>(s) * HC * (kD + 2);
+            const float l = __ldcg(pp + 1);
+            if (l > 0.f) {
+                const float f = expf(__ldcg(pp) - M);
+                L += l * f;
+                o += __ldcg(pp + 2 + e) * f;
+            }
+        }
+        const int64_t h = h0 + hh;
+        a.out[h * kD + e] = L > 0.f ? o / L : NAN;
+        if (a.part_o) a.part_o[h * kD + e] = L > 0.f ? o / L : 0.f;
+        if (e == 0 && a.part_m) { a.part_m[h] = M; a.part_l[h] = L; }
+    }
+}
+
+// ------------------------------------------------------------------ materialize
+struct MatArgs {
+    hp_list_ref ref[4];
+    const int32_t* count[4];
+    int32_t* out[4];
+    int64_t stride[4];
+};
+
+__global__ void materialize_kernel(const MatArgs a) {
+    const int l = blockIdx.z, m = blockIdx.y;
+    const int64_t n = a.count[l][m];
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        a.out[l][m * a.stride[l] + i] = static_cast<int32_t>(ref_token(a.ref[l], m, i));
+}
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+int bsa_hc(int n_q_heads, int n_kv, int hpm) {
+    const int g = n_q_heads / n_kv;
+    int hc = std::__gcd(g, hpm);
+    hc = std::__gcd(hc, kMaxHC);
+    return std::max(1, hc);
+}
+
+template <typename T, bool EXT>
+cudaError_t launch_stage(const hp_decode_stage_args& a, float* scores, int* tickets, cudaStream_t s) {
+    using G = RowGeom<T>;
+    const int hpm = a.heads_per_mask;
+    int cg = std::max(1, kStageWarps / hpm);
+    const int warps = std::min(kStageWarps, std::max(hpm * cg, 1));
+    const int threads = std::max(32, std::min(warps, hpm * cg) * 32);
+    const int nw = threads / 32;
+    const size_t smem = static_cast<size_t>(hpm) * kD * 4 + static_cast<size_t>(hpm) * 32 * cg * 4 + 128 +
+                        static_cast<size_t>(nw) * 32 * G::bytes;
+    auto kern = decode_stage_kernel<T, EXT>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    dim3 grid((a.max_chunks + 32 * cg - 1) / (32 * cg), a.n_masks);
+    kern<<<grid, threads, smem, s>>>(a, scores, tickets, cg);
+    return cudaGetLastError();
+}
+
+template <typename T, int HC, bool EXT>
+cudaError_t launch_bsa(const hp_decode_bsa_args& a, float* part, int* tickets, int splits, cudaStream_t s) {
+    dim3 grid(splits, a.n_q_heads / HC);
+    decode_bsa_kernel<T, HC, EXT><<<grid, kBsaWarps * 32, 0, s>>>(a, part, tickets, splits);
+    return cudaGetLastError();
+}
+
+template <typename T, bool EXT>
+cudaError_t dispatch_bsa_hc(const hp_decode_bsa_args& a, int hc, float* part, int* tickets, int splits, cudaStream_t s) {
+    switch (hc) {
+        case 1: return launch_bsa<T, 1, EXT>(a, part, tickets, splits, s);
+        case 2: return launch_bsa<T, 2, EXT>(a, part, tickets, splits, s);
+        case 4: return launch_bsa<T, 4, EXT>(a, part, tickets, splits, s);
+        default: return launch_bsa<T, 8, EXT>(a, part, tickets, splits, s);
+    }
+}
+
+}  // namespace
+
+extern "C" size_t hp_decode_stage_workspace_bytes(int32_t n_masks, int32_t max_chunks) {
+    return align_up(static_cast<size_t>(n_masks) * std::max(1, max_chunks) * 4, 256) +
+           align_up(static_cast<size_t>(n_masks) * 4, 256);
+}
+
+extern "C" int hp_decode_stage(const hp_decode_stage_args* ap, void* stream) {
+    if (!ap) return hph::set_error(HP_INVALID_ARGUMENT, "hp_decode_stage: null args");
+    const hp_decode_stage_args& a = *ap;
+    if (a.chunk_size <= 0) return hph::set_error(HP_INVALID_ARGUMENT, "StageConfig: b_q and l_c must be >= 1");
+    if (a.keep <= 0 || a.keep % a.chunk_size) return hph::set_error(HP_INVALID_ARGUMENT, "StageConfig: k must be a positive multiple of l_c");
+    if (a.keys.d != kD) return hph::set_error(HP_INVALID_ARGUMENT, "hp_decode_stage: fused decode path needs head_dim 128");
+    if (a.n_masks <= 0 || a.heads_per_mask <= 0 || a.heads_per_mask > 32 || a.n_q_heads != a.n_masks * a.heads_per_mask ||
+        a.keys.n_kv <= 0 || a.n_q_heads % a.keys.n_kv)
+        return hph::set_error(HP_INVALID_ARGUMENT, "hp_decode_stage: bad head geometry");
+    if (a.in.depth < 0 || a.in.depth > 4) return hph::set_error(HP_INVALID_ARGUMENT, "hp_decode_stage: list depth");
+    if (a.sel_stride < a.keep / a.chunk_size) return hph::set_error(HP_INVALID_ARGUMENT, "hp_decode_stage: sel_stride < k/l_c");
+    if (a.max_chunks <= 0) return hph::set_error(HP_INVALID_ARGUMENT, "hp_decode_stage: max_chunks must be >= 1");
+    const size_t need = hp_decode_stage_workspace_bytes(a.n_masks, a.max_chunks);
+    if (!a.workspace || a.workspace_bytes < need) return hph::set_error(HP_INVALID_ARGUMENT, "hp_decode_stage: workspace too small");
+    if (a.rope.extension) {
+        const int pol = a.rope.layer > a.rope.early_cutoff ? a.rope.late_policy : a.rope.early_policy;
+        if (pol != HP_ROPE_CHUNK_INDEXED && pol != HP_ROPE_RELATIVE)
+            return hph::set_error(HP_LOGIC_ERROR, "query_position: policy not applicable to pruning");
+        const int64_t need_q = pol == HP_ROPE_RELATIVE ? a.stream_tokens + 1 : min64(a.query_position, a.max_chunks + a.stream_tokens);
+        const int64_t need_k = pol == HP_ROPE_RELATIVE ? 1 : a.max_chunks - 1;
+        if (std::max(need_q, need_k) >= a.rope.rope_max)
+            return hph::set_error(HP_OUT_OF_RANGE, "apply_rope: position %lld >= max_position %lld",
+                                  static_cast<long long>(std::max(need_q, need_k)), static_cast<long long>(a.rope.rope_max));
+    }
+    char* ws = static_cast<char*>(a.workspace);
+    float* scores = reinterpret_cast<float*>(ws);
+    int* tickets = reinterpret_cast<int*>(ws + align_up(static_cast<size_t>(a.n_masks) * a.max_chunks * 4, 256));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const bool ext = a.rope.extension != 0;
+    cudaError_t e;
+    if (a.keys.dtype == HP_BF16) e = ext ? launch_stage<bf16_t, true>(a, scores, tickets, s) : launch_stage<bf16_t, false>(a, scores, tickets, s);
+    else e = ext ? launch_stage<float, true>(a, scores, tickets, s) : launch_stage<float, false>(a, scores, tickets, s);
+    return hph::check_cuda(e, "decode_stage_kernel");
+}
+
+extern "C" size_t hp_decode_bsa_workspace_bytes(int32_t n_q_heads, int32_t max_sel) {
+    const int splits = std::max(1, (max_sel + kBsaKeysPerCta - 1) / kBsaKeysPerCta);
+    return align_up(static_cast<size_t>(n_q_heads) * splits * (kD + 2) * 4, 256) + align_up(static_cast<size_t>(n_q_heads) * 4, 256);
+}
+
+extern "C" int hp_decode_bsa(const hp_decode_bsa_args* ap, void* stream) {
+    if (!ap) return hph::set_error(HP_INVALID_ARGUMENT, "hp_decode_bsa: null args");
+    const hp_decode_bsa_args& a = *ap;
+    if (a.kv.d != kD) return hph::set_error(HP_INVALID_ARGUMENT, "hp_decode_bsa: fused decode path needs head_dim 128");
+    if (a.n_q_heads <= 0 || a.heads_per_mask <= 0 || a.kv.n_kv <= 0 || a.n_q_heads % a.kv.n_kv || a.n_q_heads % a.heads_per_mask)
+        return hph::set_error(HP_INVALID_ARGUMENT, "hp_decode_bsa: bad head geometry");
+    if (!a.q || !a.out || !a.mask_count || !a.kv.k_pool || !a.kv.v_pool) return hph::set_error(HP_INVALID_ARGUMENT, "hp_decode_bsa: null pointer");
+    const int64_t pos = a.query_position;
+    const int64_t sink_end = std::min<int64_t>(a.sink_tokens, pos + 1);
+    const int64_t stream_begin = std::max<int64_t>(pos + 1 > a.stream_tokens ? pos + 1 - a.stream_tokens : 0, sink_end);
+    const int64_t max_sel = sink_end + a.max_mask + (pos + 1 - stream_begin);
+    if (max_sel <= 0) return hph::set_error(HP_INVALID_ARGUMENT, "attention_row: empty selected set");
+    if (a.rope.extension) {
+        if (pos >= a.rope.rope_max) return hph::set_error(HP_OUT_OF_RANGE, "apply_rope: position %lld >= max_position %lld",
+                                                          static_cast<long long>(pos), static_cast<long long>(a.rope.rope_max));
+        if (max_sel > pos + 1) return hph::set_error(HP_LOGIC_ERROR, "streaming_positions: selected tokens cannot fit below position");
+    }
+    const int splits = static_cast<int>((max_sel + kBsaKeysPerCta - 1) / kBsaKeysPerCta);
+    const size_t need = hp_decode_bsa_workspace_bytes(a.n_q_heads, static_cast<int32_t>(max_sel));
+    if (!a.workspace || a.workspace_bytes < need) return hph::set_error(HP_INVALID_ARGUMENT, "hp_decode_bsa: workspace too small");
+    char* ws = static_cast<char*>(a.workspace);
+    float* part = reinterpret_cast<float*>(ws);
+    int* tickets = reinterpret_cast<int*>(ws + align_up(static_cast<size_t>(a.n_q_heads) * splits * (kD + 2) * 4, 256));
+    const int hc = bsa_hc(a.n_q_heads, a.kv.n_kv, a.heads_per_mask);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const bool ext = a.rope.extension != 0;
+    cudaError_t e;
+    if (a.kv.dtype == HP_BF16) e = ext ? dispatch_bsa_hc<bf16_t, true>(a, hc, part, tickets, splits, s) : dispatch_bsa_hc<bf16_t, false>(a, hc, part, tickets, splits, s);
+    else e = ext ? dispatch_bsa_hc<float, true>(a, hc, part, tickets, splits, s) : dispatch_bsa_hc<float, false>(a, hc, part, tickets, splits, s);
+    return hph::check_cuda(e, "decode_bsa_kernel");
+}
+
+extern "C" int hp_decode_materialize(const hp_list_ref* refs, const int32_t* const* counts,
+                                     int32_t* const* outs, const int64_t* out_strides,
+                                     int32_t n_lists, int32_t n_masks, int32_t max_count,
+                                     void* stream) {
+    if (n_lists <= 0 || n_lists > 4 || n_masks <= 0) return hph::set_error(HP_INVALID_ARGUMENT, "hp_decode_materialize: 1..4 lists");
+    MatArgs m{};
+    for (int i = 0; i < n_lists; ++i) {
+        m.ref[i] = refs[i];
+        m.count[i] = counts[i];
+        m.out[i] = outs[i];
+        m.stride[i] = out_strides[i];
+    }
+    const int blocks = std::max(1, std::min(64, (max_count + 255) / 256));
+    materialize_kernel<<<dim3(blocks, n_masks, n_lists), 256, 0, static_cast<cudaStream_t>(stream)>>>(m);
+    return hph::check_cuda(cudaGetLastError(), "materialize_kernel");
+}

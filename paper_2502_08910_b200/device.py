@@ -365,3 +365,132 @@ class DecodeLayer:
         bsa(self.q, self.kv, self.sel, self.sel_count, query_offset=pos, max_sel=self.sel_stride,
             policy=self.policy, rope=self.rope, out=self.out, ws=self.ws, stream=stream)
         return self.out
+
+
+# ----------------------------------------------------------- fused decode (d=128)
+def _ref_range(start: int):
+    r = _capi.ListRef()
+    r.depth = 0
+    r.base_list = None
+    r.range_start = start
+    return r
+
+
+def _ref_list(base: torch.Tensor):
+    r = _capi.ListRef()
+    r.depth = 0
+    r.base_list = _ptr(base)
+    r.base_stride = base.shape[-1]
+    r.range_start = 0
+    return r
+
+
+def _ref_push(ref, sel: torch.Tensor, lc: int):
+    r = _capi.ListRef()
+    C.pointer(r)[0] = ref
+    if ref.depth >= 4:
+        raise ValueError("list chain deeper than 4 stages")
+    r.sel[ref.depth] = _ptr(sel)
+    r.sel_stride[ref.depth] = sel.shape[-1]
+    r.lc[ref.depth] = lc
+    r.depth = ref.depth + 1
+    return r
+
+
+class FusedDecodeLayer:
+    """The per-layer decode body on the fused kernels (d = 128): one kernel per due
+    stage (exact top-k fused), one BSA kernel (fused combine), one materialize
+    kernel that refreshes the stage caches (DecodeEngine::caches_, decode.hpp:107).
+
+    Stage caches follow DecodeEngine::step (decode.cpp:225-249): a due stage reads
+    the previous stage's list — implicit (chunk ids) when that stage also ran this
+    step, the materialized cache otherwise."""
+
+    def __init__(self, kv: PagedKV, stages, *, sink: int, stream_tokens: int, n_q_heads: int,
+                 n_masks: int, layer1: int = 4, policy: RopePolicy | None = None,
+                 rope: RopeTable | None = None, device="cuda"):
+        require_cuda()
+        if kv.d != 128:
+            raise ValueError("FusedDecodeLayer: head_dim must be 128 (use DecodeLayer)")
+        self.kv, self.stages = kv, [tuple(s) for s in stages]
+        self.sink, self.stream_tokens = sink, stream_tokens
+        self.n_q_heads, self.n_masks = n_q_heads, n_masks
+        self.hpm = n_q_heads // n_masks
+        self.layer1 = layer1
+        self.policy = policy or RopePolicy()
+        self.rope = rope
+        dev = self.dev = torch.device(device)
+        S = len(self.stages)
+        self.sel = [torch.zeros((n_masks, max(1, keep // lc)), dtype=torch.int32, device=dev)
+                    for (_, lc, keep) in self.stages]
+        self.count = [torch.zeros((n_masks,), dtype=torch.int32, device=dev) for _ in range(S)]
+        self.cache = [torch.zeros((n_masks, keep), dtype=torch.int32, device=dev)
+                      for (_, _, keep) in self.stages]
+        self.q = torch.zeros((n_q_heads, kv.d), dtype=torch.float32, device=dev)
+        self.out = torch.zeros((n_q_heads, kv.d), dtype=torch.float32, device=dev)
+        t_max = kv.num_pages * kv.page_size
+        n0 = max(0, t_max - stream_tokens - sink)
+        self.max_chunks = []
+        prev = n0
+        for (_, lc, keep) in self.stages:
+            self.max_chunks.append(max(1, ceil_div(prev, lc)))
+            prev = keep
+        ws_stage = max(lib().hp_decode_stage_workspace_bytes(n_masks, mc) for mc in self.max_chunks)
+        self.ws_stage = torch.zeros(ws_stage, dtype=torch.uint8, device=dev)
+        max_sel = sink + self.stages[-1][2] + stream_tokens + 1
+        self.ws_bsa = torch.zeros(lib().hp_decode_bsa_workspace_bytes(n_q_heads, max_sel),
+                                  dtype=torch.uint8, device=dev)
+        self._keep = []  # ctypes objects alive across async launches
+
+    def run(self, t: int, refresh=None, stream=None, materialize: bool = True) -> torch.Tensor:
+        S = len(self.stages)
+        refresh = list(refresh) if refresh is not None else [True] * S
+        pos = t - 1
+        upper = t - self.stream_tokens if t > self.stream_tokens else 0
+        n0 = max(0, upper - self.sink)
+        sp = C.c_void_p(_stream(stream))
+        kvv = self.kv.view(t)
+        chains = [None] * S
+        for i, (_, lc, keep) in enumerate(self.stages):
+            if i == 0:
+                in_ref, in_count, const = _ref_range(self.sink), None, n0
+            elif refresh[i - 1]:
+                in_ref, in_count, const = chains[i - 1], self.count[i - 1], 0
+            else:
+                in_ref, in_count, const = _ref_list(self.cache[i - 1]), self.count[i - 1], 0
+            if refresh[i]:
+                a = _capi.DecodeStageArgs(
+                    chunk_size=lc, keep=keep, n_masks=self.n_masks, heads_per_mask=self.hpm,
+                    n_q_heads=self.n_q_heads, stream_tokens=self.stream_tokens, q=_ptr(self.q),
+                    query_position=pos, in_=in_ref, in_count=_ptr(in_count), in_count_const=const,
+                    max_chunks=self.max_chunks[i], sel_stride=self.sel[i].shape[-1],
+                    sel_out=_ptr(self.sel[i]), out_count=_ptr(self.count[i]),
+                    workspace=_ptr(self.ws_stage), workspace_bytes=self.ws_stage.numel(),
+                    keys=kvv, rope=self.policy.ctx(self.layer1, self.rope))
+                check(lib().hp_decode_stage(C.byref(a), sp))
+                chains[i] = _ref_push(in_ref, self.sel[i], lc)
+            else:
+                chains[i] = _ref_list(self.cache[i])
+        b = _capi.DecodeBsaArgs(
+            n_q_heads=self.n_q_heads, heads_per_mask=self.hpm, sink_tokens=self.sink,
+            stream_tokens=self.stream_tokens, q=_ptr(self.q), query_position=pos,
+            mask=chains[-1], mask_count=_ptr(self.count[-1]), max_mask=self.stages[-1][2],
+            out=_ptr(self.out), part_m=None, part_l=None, part_o=None,
+            workspace=_ptr(self.ws_bsa), workspace_bytes=self.ws_bsa.numel(), kv=kvv,
+            rope=self.policy.ctx(0, self.rope))
+        check(lib().hp_decode_bsa(C.byref(b), sp))
+        if materialize:
+            idx = [i for i in range(S) if refresh[i]]
+            if idx:
+                n = len(idx)
+                refs = (_capi.ListRef * n)(*[chains[i] for i in idx])
+                counts = (C.c_void_p * n)(*[_ptr(self.count[i]) for i in idx])
+                outs = (C.c_void_p * n)(*[_ptr(self.cache[i]) for i in idx])
+                strides = (C.c_int64 * n)(*[self.cache[i].shape[-1] for i in idx])
+                check(lib().hp_decode_materialize(refs, counts, outs, strides, n, self.n_masks,
+                                                  max(self.stages[i][2] for i in idx), sp))
+        return self.out
+
+    def mask(self, stage: int = -1):
+        """Materialized stage cache (lists, counts) — DecodeEngine::stage_cache."""
+        return self.cache[stage], self.count[stage]

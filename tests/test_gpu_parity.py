@@ -259,3 +259,77 @@ def test_decode_layer_step(port, case):
         got = cl[g, 0, : int(cc[g, 0])].cpu().numpy()
         assert np.array_equal(got, masks[g]), g
     assert_close(out.cpu().numpy().reshape(groups, hpm, 128), want_out)
+
+
+@pytest.mark.parametrize("case", ["c1_32k_f32", "c1_64k_f32_ext", "gqa_128k_bf16", "gqa_1m_bf16_g1"])
+def test_fused_decode_layer_step(port, case):
+    """Fused decode kernels (one kernel per stage, fused top-k, implicit lists, fused
+    BSA combine) against the oracle's per-layer decode body."""
+    D = _dev()
+    dev = torch.device("cuda")
+    stages = [(64, 256, 32768), (64, 32, 8192), (64, 8, 2048)]
+    t, groups, hpm, bf16, ext, layer1 = {
+        "c1_32k_f32": (32768, 1, 1, False, False, 4),
+        "c1_64k_f32_ext": (65536, 1, 1, False, True, 2),
+        "gqa_128k_bf16": (131072, 2, 4, True, False, 4),
+        "gqa_1m_bf16_g1": (1 << 20, 1, 4, True, False, 4),
+    }[case]
+    q, k, v = workload(5, groups * hpm, groups, 1, t, 128, bf16=bf16)
+    dtype = torch.bfloat16 if bf16 else torch.float32
+    kv = D.PagedKV(torch.from_numpy(k), torch.from_numpy(v), page_size=64, dtype=dtype)
+    rope = D.RopeTable(t + 2, 128) if ext else None
+    layer = D.FusedDecodeLayer(kv, stages, sink=256, stream_tokens=1024, n_q_heads=groups * hpm,
+                               n_masks=groups, layer1=layer1, policy=D.RopePolicy(extension=ext),
+                               rope=rope)
+    layer.q.copy_(torch.from_numpy(q[:, 0]).to(dev))
+    for _ in range(2):  # second run checks the self-resetting tickets
+        out = layer.run(t).clone()
+        torch.cuda.synchronize()
+        masks, want_out, _ = port.decode_layer_step(q.reshape(groups, hpm, 128), k, v, stages,
+                                                    sink=256, stream=1024, ext=ext, layer1=layer1)
+        cl, cc = layer.mask()
+        for g in range(groups):
+            got = cl[g, : int(cc[g])].cpu().numpy()
+            assert np.array_equal(got, masks[g]), g
+        assert_close(out.cpu().numpy().reshape(groups, hpm, 128), want_out)
+
+
+def test_fused_decode_refresh_schedule():
+    """Stage caches across steps (decode.cpp:212-249): with intervals (4, 2, 1) the fused
+    layer must equal the generic-kernel layer driven by the same refresh flags."""
+    D = _dev()
+    dev = torch.device("cuda")
+    stages = [(1, 64, 4096), (1, 16, 1024), (1, 4, 256)]
+    t0, steps, groups, hpm = 40000, 12, 2, 4
+    q, k, v = workload(9, groups * hpm, groups, steps, t0 + steps, 128, bf16=True)
+    kvf = D.PagedKV(torch.from_numpy(k[:, :t0]), torch.from_numpy(v[:, :t0]), dtype=torch.bfloat16,
+                    capacity=t0 + steps)
+    kvg = D.PagedKV(torch.from_numpy(k[:, :t0]), torch.from_numpy(v[:, :t0]), dtype=torch.bfloat16,
+                    capacity=t0 + steps)
+    kw = dict(sink=64, stream_tokens=256, n_q_heads=groups * hpm, n_masks=groups)
+    fused = D.FusedDecodeLayer(kvf, stages, **kw)
+    generic = D.DecodeLayer(kvg, stages, **kw)
+    counters = [0, 0, 0]
+    intervals = [4, 2, 1]
+    for s in range(steps):
+        t = t0 + s + 1
+        krow = torch.from_numpy(k[:, t - 1]).to(dev)
+        vrow = torch.from_numpy(v[:, t - 1]).to(dev)
+        kvf.append(krow, vrow)
+        kvg.append(krow, vrow)
+        flags = [c == 0 for c in counters]
+        qs = torch.from_numpy(q[:, s]).to(dev)
+        fused.q.copy_(qs)
+        generic.q.copy_(qs.unsqueeze(1))
+        of = fused.run(t, refresh=flags).clone()
+        og = generic.run(t, refresh=flags).clone()
+        torch.cuda.synchronize()
+        for i in range(3):
+            fl, fc = fused.mask(i)
+            gl, gc = generic.caches[i]
+            for g in range(groups):
+                n = int(fc[g])
+                assert n == int(gc[g, 0])
+                assert torch.equal(fl[g, :n].cpu(), gl[g, 0, :n].cpu()), (s, i, g)
+        assert_close(of.cpu().numpy(), og[:, 0].cpu().numpy(), rtol=1e-5)
+        counters = [(c + 1) % iv for c, iv in zip(counters, intervals)]
