@@ -210,6 +210,11 @@ typedef struct hp_decode_stage_args {
     size_t workspace_bytes;
     hp_kv_view keys;
     hp_rope_ctx rope;
+    /* optional device int: nonzero when every key element is bf16 with |k| in
+     * [2^-63, 2^63] or 0. With bf16-exact q (checked in-kernel) every q*k product
+     * is then exact in fp32, so fma(q,k,acc) == acc + q*k bit for bit and the
+     * sequential dot issues one FFMA per element instead of FMUL + FADD. */
+    const int32_t* keys_exact;
 } hp_decode_stage_args;
 
 size_t hp_decode_stage_workspace_bytes(int32_t n_masks, int32_t max_chunks);

@@ -81,7 +81,8 @@ class DecodeStageArgs(C.Structure):
                 ("in_", ListRef), ("in_count", C.c_void_p), ("in_count_const", C.c_int64),
                 ("max_chunks", C.c_int32), ("sel_stride", C.c_int32), ("sel_out", C.c_void_p),
                 ("out_count", C.c_void_p), ("workspace", C.c_void_p),
-                ("workspace_bytes", C.c_size_t), ("keys", KvView), ("rope", RopeCtx)]
+                ("workspace_bytes", C.c_size_t), ("keys", KvView), ("rope", RopeCtx),
+                ("keys_exact", C.c_void_p)]
 
 
 class DecodeBsaArgs(C.Structure):

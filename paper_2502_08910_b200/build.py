@@ -41,14 +41,17 @@ def build_cuda(force: bool = False, verbose: bool = False) -> Path:
     deps = [CSRC / s for s in CUDA_SOURCES] + list(CSRC.glob("*.cuh")) + [ROOT / "include" / "hipprune_b200.h", Path(__file__)]
     if not force and not _stale(out, deps):
         return out
-    objs = []
-    for src in CUDA_SOURCES:
+    objs, procs = [], []
+    for src in CUDA_SOURCES:  # compile translation units in parallel
         obj = LIB / (Path(src).stem + ".o")
-        cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-dc" if False else "-c", str(CSRC / src), "-o", str(obj)]
+        cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-c", str(CSRC / src), "-o", str(obj)]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
-        subprocess.run(cmd, check=True)
+        procs.append((src, subprocess.Popen(cmd)))
         objs.append(str(obj))
+    for src, p in procs:
+        if p.wait() != 0:
+            raise RuntimeError(f"nvcc failed on {src}")
     subprocess.run([nvcc(), *ARCH, "-shared", "-Xcompiler", "-fPIC", *objs, "-o", str(out)], check=True)
     for o in objs:
         Path(o).unlink(missing_ok=True)

@@ -36,8 +36,11 @@ __device__ __forceinline__ float load_elem(const bf16_t* p, int i) {
 __device__ __forceinline__ const char* kv_row_ptr(const hp_kv_view& v, const void* pool,
                                                   const void* host, int kv, int64_t tok,
                                                   int elem_bytes) {
-    const int64_t page = tok / v.page_size;
-    const int64_t off = tok - page * v.page_size;
+    // tokens < 2^31: 32-bit page split (a shift when page_size is a power of two)
+    const uint32_t t32 = static_cast<uint32_t>(tok);
+    const uint32_t ps = static_cast<uint32_t>(v.page_size);
+    const int64_t page = (ps & (ps - 1)) == 0 ? (t32 >> (__ffs(ps) - 1)) : t32 / ps;
+    const int64_t off = t32 - static_cast<uint32_t>(page) * ps;
     int64_t slot = v.page_table ? static_cast<int64_t>(v.page_table[page]) : page;
     const bool hit = slot >= 0;
     if (v.touched) {

@@ -40,9 +40,10 @@ constexpr int kMaxHC = 8;
 __device__ __forceinline__ int64_t ref_token(const hp_list_ref& L, int mask, int64_t pos) {
 #pragma unroll 1
     for (int i = L.depth - 1; i >= 0; --i) {
-        const int64_t lc = L.lc[i];
-        const int64_t r = pos / lc;
-        pos = static_cast<int64_t>(L.sel[i][static_cast<int64_t>(mask) * L.sel_stride[i] + r]) * lc + (pos - r * lc);
+        const uint32_t lc = static_cast<uint32_t>(L.lc[i]);
+        const uint32_t p32 = static_cast<uint32_t>(pos);  // list positions < 2^31
+        const uint32_t r = p32 / lc;
+        pos = static_cast<int64_t>(L.sel[i][static_cast<int64_t>(mask) * L.sel_stride[i] + r]) * lc + (p32 - r * lc);
     }
     return L.base_list ? static_cast<int64_t>(L.base_list[mask * L.base_stride + pos]) : L.range_start + pos;
 }
@@ -70,6 +71,35 @@ __device__ __forceinline__ float dot_row<bf16_t>(const unsigned char* row, int s
         acc = __fadd_rn(acc, __fmul_rn(qb.w, bf16_hi(w.w)));
     }
     return acc;
+}
+
+// Same dot when every product q[i]*k[i] is exact in fp32 (bf16 x bf16 in range):
+// fma(q, k, acc) rounds once, exactly like acc + (q*k) with an exact product.
+__device__ __forceinline__ float dot_row_fma(const unsigned char* row, int swz, const float* q) {
+    const float4* q4 = reinterpret_cast<const float4*>(q);
+    float acc = 0.0f;
+#pragma unroll 4
+    for (int c = 0; c < 16; ++c) {
+        const uint4 w = *reinterpret_cast<const uint4*>(row + ((c ^ swz) << 4));
+        const float4 qa = q4[2 * c], qb = q4[2 * c + 1];
+        acc = __fmaf_rn(qa.x, bf16_lo(w.x), acc);
+        acc = __fmaf_rn(qa.y, bf16_hi(w.x), acc);
+        acc = __fmaf_rn(qa.z, bf16_lo(w.y), acc);
+        acc = __fmaf_rn(qa.w, bf16_hi(w.y), acc);
+        acc = __fmaf_rn(qb.x, bf16_lo(w.z), acc);
+        acc = __fmaf_rn(qb.y, bf16_hi(w.z), acc);
+        acc = __fmaf_rn(qb.z, bf16_lo(w.w), acc);
+        acc = __fmaf_rn(qb.w, bf16_hi(w.w), acc);
+    }
+    return acc;
+}
+
+// q is bf16-exact with |q| in [2^-63, 2^63] or 0 (so bf16 products stay exact).
+__device__ __forceinline__ bool q_product_safe(float x) {
+    const uint32_t u = __float_as_uint(x);
+    if ((u & 0xffffu) != 0u) return false;
+    const float ax = fabsf(x);
+    return ax == 0.0f || (ax >= 1.0842022e-19f && ax <= 9.2233720e18f);
 }
 
 template <>
@@ -182,7 +212,20 @@ __device__ void cta_topk(const float* sc, int64_t cc, int K, int32_t* sel_out, u
     const int nt = blockDim.x;
     const bool in_smem = cc <= smem_cap;
     if (in_smem) {
-        for (int64_t j = threadIdx.x; j < cc; j += nt) skeys[j] = order_key(__ldcg(sc + j));
+        // batched loads: 8 independent L2 reads in flight per thread
+        for (int64_t b0 = 0; b0 < cc; b0 += 8 * nt) {
+            float v[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int64_t j = b0 + k * nt + threadIdx.x;
+                v[k] = j < cc ? __ldcg(sc + j) : 0.f;
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int64_t j = b0 + k * nt + threadIdx.x;
+                if (j < cc) skeys[j] = order_key(v[k]);
+            }
+        }
         __syncthreads();
     }
     auto key = [&](int64_t j) -> uint32_t { return in_smem ? skeys[j] : order_key(__ldcg(sc + j)); };
@@ -191,9 +234,15 @@ __device__ void cta_topk(const float* sc, int64_t cc, int K, int32_t* sel_out, u
     for (int shift = 24; shift >= 0; shift -= 8) {
         for (int i = threadIdx.x; i < 256; i += nt) hist[i] = 0;
         __syncthreads();
-        for (int64_t j = threadIdx.x; j < cc; j += nt) {
-            const uint32_t u = key(j);
-            if ((u & pmask) == prefix) atomicAdd(&hist[(u >> shift) & 255u], 1);
+        // warp-aggregated: chunk scores cluster in few bins, so same-bin lanes merge
+        // their increments (__match_any) instead of serialising on one address
+        for (int64_t b0 = 0; b0 < cc; b0 += nt) {
+            const int64_t j = b0 + threadIdx.x;
+            const uint32_t u = j < cc ? key(j) : 0u;
+            const bool act = j < cc && (u & pmask) == prefix;
+            const int bin = act ? static_cast<int>((u >> shift) & 255u) : 256;
+            const unsigned peers = __match_any_sync(0xffffffffu, bin);
+            if (act && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&hist[bin], __popc(peers));
         }
         __syncthreads();
         if (threadIdx.x < 32) {
@@ -267,13 +316,20 @@ decode_stage_kernel(const hp_decode_stage_args a, float* scores, int* tickets, i
     if (chunk0 >= cc) return;
 
     const int nwarps = blockDim.x >> 5;
-    float* qs = reinterpret_cast<float*>(smem);                       // [hpm][128]
+    // staging first so every derived pointer stays a shared-window pointer (LDS, not LD.E)
+    unsigned char* stage = smem;                                      // [nwarps][32][row]
+    float* qs = reinterpret_cast<float*>(smem + static_cast<size_t>(nwarps) * 32 * G::bytes);  // [hpm][128]
     float* red = qs + hpm * kD;                                       // [hpm][chunks_per_cta]
-    unsigned char* stage = reinterpret_cast<unsigned char*>(red + hpm * chunks_per_cta);
-    stage = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(stage) + 127) & ~uintptr_t(127));
 
-    for (int i = threadIdx.x; i < hpm * kD; i += blockDim.x) qs[i] = a.q[static_cast<int64_t>(m * hpm) * kD + i];
-    __syncthreads();
+    bool q_safe = true;
+    for (int i = threadIdx.x; i < hpm * kD; i += blockDim.x) {
+        const float x = a.q[static_cast<int64_t>(m * hpm) * kD + i];
+        qs[i] = x;
+        q_safe &= q_product_safe(x);
+    }
+    // FFMA path only without rotation, with bf16 keys certified in range, and bf16-exact q
+    const bool use_fma = __syncthreads_and(q_safe) && !EXT && sizeof(T) == 2 &&
+                         a.keys_exact != nullptr && *a.keys_exact != 0;
     if constexpr (EXT) {
         constexpr int half = kD / 2;
         const int64_t qp = rope_q_position(a.rope, a.query_position, a.stream_tokens, cc);
@@ -328,7 +384,7 @@ decode_stage_kernel(const hp_decode_stage_args a, float* scores, int* tickets, i
                 s1 = dot_row_rot<T>(myrow, swz, qrow, cs1, sn1);
                 s2 = same_rot ? s1 : dot_row_rot<T>(myrow, swz, qrow, cs2, sn2);
             } else {
-                s1 = s2 = dot_row<T>(myrow, swz, qrow);
+                s1 = s2 = use_fma ? dot_row_fma(myrow, swz, qrow) : dot_row<T>(myrow, swz, qrow);
             }
         }
         for (;;) {
@@ -343,7 +399,7 @@ decode_stage_kernel(const hp_decode_stage_args a, float* scores, int* tickets, i
                     m1 = dot_row_rot<T>(myrow, swz, qrow, cs1, sn1);
                     m2 = same_rot ? m1 : dot_row_rot<T>(myrow, swz, qrow, cs2, sn2);
                 } else {
-                    m1 = m2 = dot_row<T>(myrow, swz, qrow);
+                    m1 = m2 = use_fma ? dot_row_fma(myrow, swz, qrow) : dot_row<T>(myrow, swz, qrow);
                 }
                 if (m2 > s1) { first = mid; s1 = m1; s2 = m2; } else { last = mid - 1; }
                 ++it;
@@ -546,23 +602,64 @@ decode_bsa_kernel(const hp_decode_bsa_args a, float* part, int* tickets, int spl
     __syncthreads();
     if (!sh_last) return;
     __threadfence();
-    // merge all splits of this head group (log-sum-exp)
+    // Merge all splits of this head group (log-sum-exp). Phase 1 pulls every (m, l)
+    // in one parallel load, phase 2 forms per-split weights, phase 3 streams the o's
+    // with independent (pipelined) loads.
+    constexpr int kMaxSplitsSmem = 128;
+    float* wgt = &sm_o[0][0][0];                  // reuse: [kMaxSplitsSmem][HC] weights
+    float* ml = wgt + kMaxSplitsSmem * HC;        // [splits][HC][2]
+    const bool fits = splits <= kMaxSplitsSmem && 3 * kMaxSplitsSmem * HC <= kBsaWarps * HC * kD;
+    const float* pbase = part + static_cast<int64_t>(hg) * splits * HC * (kD + 2);
+    if (fits) {
+        for (int i = threadIdx.x; i < splits * HC; i += blockDim.x) {
+            const float* pp = pbase + static_cast<int64_t>(i) * (kD + 2);
+            ml[2 * i] = __ldcg(pp);
+            ml[2 * i + 1] = __ldcg(pp + 1);
+        }
+        __syncthreads();
+        if (w < HC) {
+            const int hh = w;
+            float M = -INFINITY;
+            for (int s = lane; s < splits; s += 32)
+                if (ml[2 * (s * HC + hh) + 1] > 0.f) M = fmaxf(M, ml[2 * (s * HC + hh)]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+            float L = 0.f;
+            for (int s = lane; s < splits; s += 32) {
+                const float l = ml[2 * (s * HC + hh) + 1];
+                const float f = l > 0.f ? expf(ml[2 * (s * HC + hh)] - M) : 0.f;
+                wgt[s * HC + hh] = f;
+                L += l * f;
+            }
+            L = warp_sum(L);
+            if (lane == 0) { sm_m[0][hh] = M; sm_l[0][hh] = L; }
+        }
+        __syncthreads();
+    }
     for (int idx = threadIdx.x; idx < HC * kD; idx += blockDim.x) {
         const int hh = idx / kD, e = idx - hh * kD;
-        const float* pb = part + (static_cast<int64_t>(hg) * splits * HC + hh) * (kD + 2);
-        float M = -INFINITY;
-        for (int s = 0; s < splits; ++s) {
-            const float* pp = pb + static_cast<int64_t>(s) * HC * (kD + 2);
-            if (__ldcg(pp + 1) > 0.f) M = fmaxf(M, __ldcg(pp));
-        }
-        float L = 0.f, o = 0.f;
-        for (int s = 0; s < splits; ++s) {
-            const float* pp = pb + static_cast<int64_t>(s) * HC * (kD + 2);
-            const float l = __ldcg(pp + 1);
-            if (l > 0.f) {
-                const float f = expf(__ldcg(pp) - M);
-                L += l * f;
-                o += __ldcg(pp + 2 + e) * f;
+        const float* pb = pbase + static_cast<int64_t>(hh) * (kD + 2);
+        float M, L, o = 0.f;
+        if (fits) {
+            M = sm_m[0][hh];
+            L = sm_l[0][hh];
+#pragma unroll 8
+            for (int s = 0; s < splits; ++s) o += __ldcg(pb + static_cast<int64_t>(s) * HC * (kD + 2) + 2 + e) * wgt[s * HC + hh];
+        } else {
+            M = -INFINITY;
+            for (int s = 0; s < splits; ++s) {
+                const float* pp = pb + static_cast<int64_t>(s) * HC * (kD + 2);
+                if (__ldcg(pp + 1) > 0.f) M = fmaxf(M, __ldcg(pp));
+            }
+            L = 0.f;
+            for (int s = 0; s < splits; ++s) {
+                const float* pp = pb + static_cast<int64_t>(s) * HC * (kD + 2);
+                const float l = __ldcg(pp + 1);
+                if (l > 0.f) {
+                    const float f = expf(__ldcg(pp) - M);
+                    L += l * f;
+                    o += __ldcg(pp + 2 + e) * f;
+                }
             }
         }
         const int64_t h = h0 + hh;
@@ -664,8 +761,10 @@ extern "C" int hp_decode_stage(const hp_decode_stage_args* ap, void* stream) {
                                   static_cast<long long>(std::max(need_q, need_k)), static_cast<long long>(a.rope.rope_max));
     }
     char* ws = static_cast<char*>(a.workspace);
-    float* scores = reinterpret_cast<float*>(ws);
-    int* tickets = reinterpret_cast<int*>(ws + align_up(static_cast<size_t>(a.n_masks) * a.max_chunks * 4, 256));
+    // tickets first: a fixed offset for every stage sharing this workspace (they must
+    // stay zero between launches; the scores region size varies per stage)
+    int* tickets = reinterpret_cast<int*>(ws);
+    float* scores = reinterpret_cast<float*>(ws + align_up(static_cast<size_t>(a.n_masks) * 4, 256));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const bool ext = a.rope.extension != 0;
     cudaError_t e;
@@ -700,8 +799,8 @@ extern "C" int hp_decode_bsa(const hp_decode_bsa_args* ap, void* stream) {
     const size_t need = hp_decode_bsa_workspace_bytes(a.n_q_heads, static_cast<int32_t>(max_sel));
     if (!a.workspace || a.workspace_bytes < need) return hph::set_error(HP_INVALID_ARGUMENT, "hp_decode_bsa: workspace too small");
     char* ws = static_cast<char*>(a.workspace);
-    float* part = reinterpret_cast<float*>(ws);
-    int* tickets = reinterpret_cast<int*>(ws + align_up(static_cast<size_t>(a.n_q_heads) * splits * (kD + 2) * 4, 256));
+    int* tickets = reinterpret_cast<int*>(ws);
+    float* part = reinterpret_cast<float*>(ws + align_up(static_cast<size_t>(a.n_q_heads) * 4, 256));
     const int hc = bsa_hc(a.n_q_heads, a.kv.n_kv, a.heads_per_mask);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const bool ext = a.rope.extension != 0;

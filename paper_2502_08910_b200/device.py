@@ -71,6 +71,16 @@ class PagedKV:
         self.v_pool = self._pack(v, device) if v is not None else None
         self.page_table = None
         self.touched = None
+        # device flag: every key is bf16 with |k| in [2^-63, 2^63] or 0, so bf16 q*k
+        # products are exact in fp32 (lets the fused stage issue FFMA, see decode.cu)
+        self.keys_exact = torch.zeros(1, dtype=torch.int32, device=device)
+        if dtype == torch.bfloat16:
+            self.keys_exact.fill_(int(self._products_safe(self.k_pool)))
+
+    @staticmethod
+    def _products_safe(x: torch.Tensor) -> bool:
+        a = x.float().abs()
+        return bool(((a == 0) | ((a >= 2.0 ** -63) & (a <= 2.0 ** 63))).all())
 
     def _pack(self, x: torch.Tensor, device) -> torch.Tensor:
         n_kv, t, d = x.shape
@@ -92,6 +102,10 @@ class PagedKV:
         if page >= self.num_pages:
             raise IndexError("PagedKV: capacity exhausted")
         self.k_pool[page, :, off].copy_(k_row)
+        if self.dtype == torch.bfloat16:
+            a = self.k_pool[page, :, off].float().abs()
+            ok = ((a == 0) | ((a >= 2.0 ** -63) & (a <= 2.0 ** 63))).all().to(torch.int32)
+            self.keys_exact.mul_(ok)
         if v_row is not None and self.v_pool is not None:
             self.v_pool[page, :, off].copy_(v_row)
         self.t_kv = t + 1
@@ -466,7 +480,8 @@ class FusedDecodeLayer:
                     max_chunks=self.max_chunks[i], sel_stride=self.sel[i].shape[-1],
                     sel_out=_ptr(self.sel[i]), out_count=_ptr(self.count[i]),
                     workspace=_ptr(self.ws_stage), workspace_bytes=self.ws_stage.numel(),
-                    keys=kvv, rope=self.policy.ctx(self.layer1, self.rope))
+                    keys=kvv, rope=self.policy.ctx(self.layer1, self.rope),
+                    keys_exact=_ptr(self.kv.keys_exact))
                 check(lib().hp_decode_stage(C.byref(a), sp))
                 chains[i] = _ref_push(in_ref, self.sel[i], lc)
             else:

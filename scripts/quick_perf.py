@@ -14,8 +14,9 @@ kv = D.PagedKV(k, v, page_size=64, dtype=torch.bfloat16)
 del k, v
 torch.cuda.synchronize()
 print(f"gen {time.time()-t0:.1f}s", flush=True)
-layer = D.DecodeLayer(kv, stages, sink=256, stream_tokens=1024, n_q_heads=groups * hpm, n_masks=groups)
-layer.q.copy_(q)
+fused = "--generic" not in sys.argv
+layer = (D.FusedDecodeLayer if fused else D.DecodeLayer)(kv, stages, sink=256, stream_tokens=1024, n_q_heads=groups * hpm, n_masks=groups)
+layer.q.copy_(q.view(layer.q.shape))
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 variants = {"full": [True] * 3, "s23_bsa": [False, True, True], "s3_bsa": [False, False, True],
             "bsa": [False] * 3}
@@ -50,4 +51,4 @@ def timeit(g, n=20):
     return ts[len(ts) // 2]
 for name, g in graphs.items():
     print(f"{name:10s} graph us (median, L2 flushed): {timeit(g):8.1f}")
-print("counts", [c.view(-1).tolist()[:2] for _, c in layer.caches], layer.sel_count.view(-1).tolist()[:2])
+print("counts", [c.view(-1).tolist()[:2] for c in layer.count] if fused else "")
