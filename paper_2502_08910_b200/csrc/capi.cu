@@ -32,6 +32,8 @@ int check_cuda(cudaError_t e, const char* what) {
 
 extern "C" const char* hp_last_error(void) { return g_error.c_str(); }
 
+
+
 extern "C" int hp_version(void) { return 1; }
 
 extern "C" int hp_device_available(void) {

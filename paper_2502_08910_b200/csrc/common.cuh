@@ -118,6 +118,24 @@ __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
 
+// ---- phase tracer (off unless hp_trace_enable set a buffer) ------------------------
+// Per-CTA %globaltimer stamps at named checkpoints of one kernel id, 8 slots per CTA.
+// internal linkage: each translation unit that traces exports its own enable call
+static __device__ unsigned long long* g_trace_buf = nullptr;
+static __device__ int g_trace_kernel = -1;
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void trace(int kernel_id, int slot) {
+    unsigned long long* b = g_trace_buf;
+    if (b != nullptr && g_trace_kernel == kernel_id && threadIdx.x == 0) {
+        const unsigned cta = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+        b[cta * 8 + slot] = globaltimer();
+    }
+}
+
 }  // namespace hpk
 
 // host-side error plumbing shared by the C-ABI translation units

@@ -156,9 +156,18 @@ struct RowGeom {
 };
 
 // Gather one key row per active lane into the warp's swizzled staging area.
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+// Optionally warms L2 with the lane's two possible next-step rows (pf0/pf1, -1 = none)
+// while this step's gather is in flight: the descent direction is unknown until the
+// compare, but both candidates are (used for latency-bound stages only — it costs
+// one wasted row per step in DRAM traffic).
 template <typename T>
 __device__ __forceinline__ void stage_rows(const hp_kv_view& kv, int kvh, int64_t tok,
-                                           unsigned char* ks, int lane) {
+                                           unsigned char* ks, int lane, int64_t pf0 = -1,
+                                           int64_t pf1 = -1) {
     using G = RowGeom<T>;
     const char* p = tok >= 0 ? kv_row_ptr(kv, kv.k_pool, kv.k_host, kvh, tok, sizeof(T)) : nullptr;
     const unsigned long long pu = reinterpret_cast<unsigned long long>(p);
@@ -169,6 +178,16 @@ __device__ __forceinline__ void stage_rows(const hp_kv_view& kv, int kvh, int64_
         const unsigned long long pp = __shfl_sync(0xffffffffu, pu, row);
         if (pp) cp_async16(ks + row * G::bytes + ((c ^ (row & (G::chunks - 1))) << 4),
                            reinterpret_cast<const char*>(pp) + (c << 4));
+    }
+    if (pf0 >= 0) {
+        const char* q0 = kv_row_ptr(kv, kv.k_pool, kv.k_host, kvh, pf0, sizeof(T));
+#pragma unroll
+        for (int o = 0; o < G::bytes; o += 128) prefetch_l2(q0 + o);
+    }
+    if (pf1 >= 0) {
+        const char* q1 = kv_row_ptr(kv, kv.k_pool, kv.k_host, kvh, pf1, sizeof(T));
+#pragma unroll
+        for (int o = 0; o < G::bytes; o += 128) prefetch_l2(q1 + o);
     }
     cp_async_wait_all();
     __syncwarp();
@@ -228,21 +247,36 @@ __device__ void cta_topk(const float* sc, int64_t cc, int K, int32_t* sel_out, u
         }
         __syncthreads();
     }
-    auto key = [&](int64_t j) -> uint32_t { return in_smem ? skeys[j] : order_key(__ldcg(sc + j)); };
+    // Radix select on v = key - kmin: chunk scores of one mask span a narrow range, so
+    // digits start at the highest bit that differs and the bins spread out (plain
+    // shared atomics, no same-address serialisation). Order is unchanged by the shift.
+    __shared__ uint32_t sh_min, sh_max;
+    uint32_t lmin = 0xffffffffu, lmax = 0u;
+    for (int64_t j = threadIdx.x; j < cc; j += nt) {
+        const uint32_t u = in_smem ? skeys[j] : order_key(__ldcg(sc + j));
+        lmin = min(lmin, u);
+        lmax = max(lmax, u);
+    }
+    lmin = __reduce_min_sync(0xffffffffu, lmin);
+    lmax = __reduce_max_sync(0xffffffffu, lmax);
+    if (threadIdx.x == 0) { sh_min = 0xffffffffu; sh_max = 0u; }
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) { atomicMin(&sh_min, lmin); atomicMax(&sh_max, lmax); }
+    __syncthreads();
+    const uint32_t kmin = sh_min, range = sh_max - sh_min;
+    auto key = [&](int64_t j) -> uint32_t { return (in_smem ? skeys[j] : order_key(__ldcg(sc + j))) - kmin; };
     uint32_t prefix = 0, pmask = 0;
     int need = K;
-    for (int shift = 24; shift >= 0; shift -= 8) {
+    const int hb = range ? 31 - __clz(range) : 0;  // highest differing bit
+    for (int shift = hb >= 7 ? hb - 7 : 0;; shift -= 8) {
+        const int s = shift < 0 ? 0 : shift;
+        const int nbits = shift < 0 ? 8 + shift : 8;
+        const uint32_t dmask = (1u << nbits) - 1u;
         for (int i = threadIdx.x; i < 256; i += nt) hist[i] = 0;
         __syncthreads();
-        // warp-aggregated: chunk scores cluster in few bins, so same-bin lanes merge
-        // their increments (__match_any) instead of serialising on one address
-        for (int64_t b0 = 0; b0 < cc; b0 += nt) {
-            const int64_t j = b0 + threadIdx.x;
-            const uint32_t u = j < cc ? key(j) : 0u;
-            const bool act = j < cc && (u & pmask) == prefix;
-            const int bin = act ? static_cast<int>((u >> shift) & 255u) : 256;
-            const unsigned peers = __match_any_sync(0xffffffffu, bin);
-            if (act && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&hist[bin], __popc(peers));
+        for (int64_t j = threadIdx.x; j < cc; j += nt) {
+            const uint32_t u = key(j);
+            if ((u & pmask) == prefix) atomicAdd(&hist[(u >> s) & dmask], 1);
         }
         __syncthreads();
         if (threadIdx.x < 32) {
@@ -264,10 +298,11 @@ __device__ void cta_topk(const float* sc, int64_t cc, int K, int32_t* sel_out, u
             }
         }
         __syncthreads();
-        prefix |= static_cast<uint32_t>(sh_digit) << shift;
-        pmask |= 255u << shift;
+        prefix |= static_cast<uint32_t>(sh_digit) << s;
+        pmask |= dmask << s;
         need -= sh_above;
         __syncthreads();
+        if (s == 0) break;
     }
     // Each thread owns a contiguous run of chunk indices so ranks follow index order.
     const int64_t per = (cc + nt - 1) / nt;
@@ -294,7 +329,7 @@ __device__ void cta_topk(const float* sc, int64_t cc, int K, int32_t* sel_out, u
 // ------------------------------------------------------------------ stage kernel
 template <typename T, bool EXT>
 __global__ void __launch_bounds__(kStageWarps * 32, 7)
-decode_stage_kernel(const hp_decode_stage_args a, float* scores, int* tickets, int cg) {
+decode_stage_kernel(const hp_decode_stage_args a, float* scores, int* tickets, int cg, int prefetch) {
     extern __shared__ __align__(128) unsigned char smem[];
     using G = RowGeom<T>;
     const int hpm = a.heads_per_mask;
@@ -314,6 +349,7 @@ decode_stage_kernel(const hp_decode_stage_args a, float* scores, int* tickets, i
         return;
     }
     if (chunk0 >= cc) return;
+    trace(10 + lc, 0);
 
     const int nwarps = blockDim.x >> 5;
     // staging first so every derived pointer stays a shared-window pointer (LDS, not LD.E)
@@ -328,6 +364,7 @@ decode_stage_kernel(const hp_decode_stage_args a, float* scores, int* tickets, i
         q_safe &= q_product_safe(x);
     }
     // FFMA path only without rotation, with bf16 keys certified in range, and bf16-exact q
+    trace(10 + lc, 1);
     const bool use_fma = __syncthreads_and(q_safe) && !EXT && sizeof(T) == 2 &&
                          a.keys_exact != nullptr && *a.keys_exact != 0;
     if constexpr (EXT) {
@@ -378,7 +415,9 @@ decode_stage_kernel(const hp_decode_stage_args a, float* scores, int* tickets, i
         int first = 1, last = len, it = 0, iters = 0;
         while ((1 << iters) < len) ++iters;
         float s1 = 0.f, s2 = 0.f;
-        stage_rows<T>(a.keys, kvh, active ? token(0) : -1, ks, lane);
+        const int mid0 = (1 + len + 1) >> 1;  // first step's mid is known up front
+        stage_rows<T>(a.keys, kvh, active ? token(0) : -1, ks, lane,
+                      prefetch && active && iters > 0 ? token(mid0 - 1) : -1);
         if (active) {
             if constexpr (EXT) {
                 s1 = dot_row_rot<T>(myrow, swz, qrow, cs1, sn1);
@@ -392,7 +431,12 @@ decode_stage_kernel(const hp_decode_stage_args a, float* scores, int* tickets, i
             if (!__any_sync(0xffffffffu, go)) break;
             const int mid = (first + last + 1) >> 1;
             __syncwarp();
-            stage_rows<T>(a.keys, kvh, go ? token(mid - 1) : -1, ks, lane);
+            int64_t pf_r = -1, pf_l = -1;
+            if (prefetch && go && it + 1 < iters) {
+                if (mid < last) pf_r = token(((mid + last + 1) >> 1) - 1);       // if it goes right
+                if (first < mid - 1) pf_l = token(((first + mid) >> 1) - 1);     // if it goes left
+            }
+            stage_rows<T>(a.keys, kvh, go ? token(mid - 1) : -1, ks, lane, pf_r, pf_l);
             if (go) {
                 float m1, m2;
                 if constexpr (EXT) {
@@ -419,6 +463,7 @@ decode_stage_kernel(const hp_decode_stage_args a, float* scores, int* tickets, i
         }
         scores[static_cast<int64_t>(m) * a.max_chunks + jj] = best;
     }
+    trace(10 + lc, 2);
     // last CTA of this mask runs the selection
     __shared__ int sh_last;
     __threadfence();
@@ -430,7 +475,9 @@ decode_stage_kernel(const hp_decode_stage_args a, float* scores, int* tickets, i
         if (sh_last) tickets[m] = 0;  // self-reset for the next launch / graph replay
     }
     __syncthreads();
+    trace(10 + lc, 3);
     if (!sh_last) return;
+    trace(10 + lc, 4);
     __threadfence();
     const int smem_cap = static_cast<int>((static_cast<size_t>(nwarps) * 32 * G::bytes) / 4);
     int32_t* sel = a.sel_out + static_cast<int64_t>(m) * a.sel_stride;
@@ -440,6 +487,7 @@ decode_stage_kernel(const hp_decode_stage_args a, float* scores, int* tickets, i
         const int64_t lastc = sel[K - 1];
         a.out_count[m] = static_cast<int32_t>(static_cast<int64_t>(K - 1) * lc + min64(lc, n_in - lastc * lc));
     }
+    trace(10 + lc, 5);
 }
 
 // -------------------------------------------------------------------- BSA kernel
@@ -467,7 +515,7 @@ template <> struct Pair<float> {
 // HC q-heads sharing one kv head and one mask. Lane L holds elements 2L, 2L+1 and
 // their RoPE partners 64+2L, 65+2L. The last CTA of each head group merges.
 template <typename T, int HC, bool EXT>
-__global__ void __launch_bounds__(kBsaWarps * 32, 2)
+__global__ void __launch_bounds__(kBsaWarps * 32, 3)
 decode_bsa_kernel(const hp_decode_bsa_args a, float* part, int* tickets, int splits) {
     using P = Pair<T>;
     __shared__ float sm_m[kBsaWarps][HC], sm_l[kBsaWarps][HC];
@@ -503,6 +551,7 @@ decode_bsa_kernel(const hp_decode_bsa_args a, float* part, int* tickets, int spl
         qx[hh][0] = x0; qx[hh][1] = x1; qy[hh][0] = y0; qy[hh][1] = y1;
     }
 
+    trace(2, 0);
     // this warp's 8 positions
     const int64_t p0 = static_cast<int64_t>(split) * kBsaKeysPerCta + w * kBsaKeysPerWarp;
     int64_t tok_l = -1;
@@ -530,6 +579,7 @@ decode_bsa_kernel(const hp_decode_bsa_args a, float* part, int* tickets, int spl
             kr[k][0] = kr[k][1] = vr[k][0] = vr[k][1] = typename P::V{};
         }
     }
+    trace(2, 1);
     float kx[kBsaKeysPerWarp][2], ky[kBsaKeysPerWarp][2];
 #pragma unroll
     for (int k = 0; k < kBsaKeysPerWarp; ++k) {
@@ -573,6 +623,7 @@ decode_bsa_kernel(const hp_decode_bsa_args a, float* part, int* tickets, int spl
         sm_o[w][hh][half + 2 * lane] = o2; sm_o[w][hh][half + 2 * lane + 1] = o3;
     }
     __syncthreads();
+    trace(2, 2);
     // CTA partial per head -> workspace [hg][split][hh][2 + 128]
     for (int idx = threadIdx.x; idx < HC * kD; idx += blockDim.x) {
         const int hh = idx / kD, e = idx - hh * kD;
@@ -600,7 +651,9 @@ decode_bsa_kernel(const hp_decode_bsa_args a, float* part, int* tickets, int spl
         if (sh_last) tickets[hg] = 0;
     }
     __syncthreads();
+    trace(2, 6);
     if (!sh_last) return;
+    trace(2, 3);
     __threadfence();
     // Merge all splits of this head group (log-sum-exp). Phase 1 pulls every (m, l)
     // in one parallel load, phase 2 forms per-split weights, phase 3 streams the o's
@@ -643,8 +696,20 @@ decode_bsa_kernel(const hp_decode_bsa_args a, float* part, int* tickets, int spl
         if (fits) {
             M = sm_m[0][hh];
             L = sm_l[0][hh];
-#pragma unroll 8
-            for (int s = 0; s < splits; ++s) o += __ldcg(pb + static_cast<int64_t>(s) * HC * (kD + 2) + 2 + e) * wgt[s * HC + hh];
+            constexpr int kBatch = 16;  // independent loads in flight per thread
+            for (int s0 = 0; s0 < splits; s0 += kBatch) {
+                float vals[kBatch];
+#pragma unroll
+                for (int k = 0; k < kBatch; ++k) {
+                    const int s = s0 + k;
+                    vals[k] = s < splits ? __ldcg(pb + static_cast<int64_t>(s) * HC * (kD + 2) + 2 + e) : 0.f;
+                }
+#pragma unroll
+                for (int k = 0; k < kBatch; ++k) {
+                    const int s = s0 + k;
+                    if (s < splits) o += vals[k] * wgt[s * HC + hh];
+                }
+            }
         } else {
             M = -INFINITY;
             for (int s = 0; s < splits; ++s) {
@@ -667,6 +732,7 @@ decode_bsa_kernel(const hp_decode_bsa_args a, float* part, int* tickets, int spl
         if (a.part_o) a.part_o[h * kD + e] = L > 0.f ? o / L : 0.f;
         if (e == 0 && a.part_m) { a.part_m[h] = M; a.part_l[h] = L; }
     }
+    trace(2, 4);
 }
 
 // ------------------------------------------------------------------ materialize
@@ -708,7 +774,10 @@ cudaError_t launch_stage(const hp_decode_stage_args& a, float* scores, int* tick
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     dim3 grid((a.max_chunks + 32 * cg - 1) / (32 * cg), a.n_masks);
-    kern<<<grid, threads, smem, s>>>(a, scores, tickets, cg);
+    // speculative next-row prefetch only where the stage is latency-bound (few descents)
+    const int64_t lanes = static_cast<int64_t>(a.n_masks) * a.max_chunks * hpm;
+    const int prefetch = lanes <= 65536 ? 1 : 0;
+    kern<<<grid, threads, smem, s>>>(a, scores, tickets, cg, prefetch);
     return cudaGetLastError();
 }
 
@@ -730,6 +799,13 @@ cudaError_t dispatch_bsa_hc(const hp_decode_bsa_args& a, int hc, float* part, in
 }
 
 }  // namespace
+
+// Developer instrumentation: record per-CTA phase stamps of kernel `kernel_id`
+// (1 = decode stage, 2 = decode BSA) into buf [n_cta][8] (NULL disables).
+extern "C" int hp_trace_enable(unsigned long long* buf, int kernel_id) {
+    if (int rc = hph::check_cuda(cudaMemcpyToSymbol(g_trace_buf, &buf, sizeof(buf)), "hp_trace_enable")) return rc;
+    return hph::check_cuda(cudaMemcpyToSymbol(g_trace_kernel, &kernel_id, sizeof(int)), "hp_trace_enable");
+}
 
 extern "C" size_t hp_decode_stage_workspace_bytes(int32_t n_masks, int32_t max_chunks) {
     return align_up(static_cast<size_t>(n_masks) * std::max(1, max_chunks) * 4, 256) +

@@ -1,0 +1,50 @@
+"""Per-CTA phase timeline of the fused decode kernels at 1M ctx (dev tool).
+Stage kernels trace as id 10 + l_c; the BSA kernel as id 2."""
+import ctypes as C
+import sys
+
+import numpy as np
+import torch
+
+from paper_2502_08910_b200 import _capi, device as D, synth
+
+t = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 20
+groups, hpm, d = 8, 4, 128
+stages = [(64, 256, 32768), (64, 32, 8192), (64, 8, 2048)]
+q, k, v = synth.generate(groups * hpm, groups, t, d, seed=1)
+kv = D.PagedKV(k, v, page_size=64, dtype=torch.bfloat16)
+del k, v
+layer = D.FusedDecodeLayer(kv, stages, sink=256, stream_tokens=1024, n_q_heads=groups * hpm, n_masks=groups)
+layer.q.copy_(q.view(layer.q.shape))
+L = _capi.lib()
+L.hp_trace_enable.argtypes = [C.c_void_p, C.c_int]
+buf = torch.zeros((8192, 8), dtype=torch.int64, device="cuda")
+flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+for _ in range(3):
+    layer.run(t)
+torch.cuda.synchronize()
+names = {10 + 256: "stage1", 10 + 32: "stage2", 10 + 8: "stage3", 2: "bsa"}
+for kid, name in names.items():
+    buf.zero_()
+    _capi.check(L.hp_trace_enable(buf.data_ptr(), kid))
+    flush.zero_()
+    torch.cuda.synchronize()
+    layer.run(t)
+    torch.cuda.synchronize()
+    _capi.check(L.hp_trace_enable(None, -1))
+    b = buf.cpu().numpy().astype(np.float64)
+    used = b[:, 0] > 0
+    b = b[used]
+    t0 = b[:, 0].min()
+    rel = np.where(b > 0, (b - t0) / 1000.0, np.nan)  # us
+    print(f"== {name}: {used.sum()} CTAs traced")
+    for s in range(8):
+        col = rel[:, s]
+        col = col[~np.isnan(col)]
+        if col.size:
+            print(f"  slot {s}: n={col.size:5d} min {col.min():8.2f} p50 {np.median(col):8.2f} "
+                  f"p90 {np.percentile(col, 90):8.2f} max {col.max():8.2f} us")
+    dur = rel[:, 3 if name != "bsa" else 6] - rel[:, 0]
+    dur = dur[~np.isnan(dur)]
+    if dur.size:
+        print(f"  per-CTA (0->ticket) p50 {np.median(dur):.2f} p90 {np.percentile(dur, 90):.2f} max {dur.max():.2f} us")
