@@ -215,6 +215,10 @@ typedef struct hp_decode_stage_args {
      * is then exact in fp32, so fma(q,k,acc) == acc + q*k bit for bit and the
      * sequential dot issues one FFMA per element instead of FMUL + FADD. */
     const int32_t* keys_exact;
+    /* optional: also write the stage's output token list, list_out[m*stride + i] for
+     * i < out_count[m] (resolved through `in`), so a consumer needs no chain hops */
+    int32_t* list_out;
+    int64_t list_out_stride;
 } hp_decode_stage_args;
 
 size_t hp_decode_stage_workspace_bytes(int32_t n_masks, int32_t max_chunks);

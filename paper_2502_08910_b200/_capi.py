@@ -82,7 +82,8 @@ class DecodeStageArgs(C.Structure):
                 ("max_chunks", C.c_int32), ("sel_stride", C.c_int32), ("sel_out", C.c_void_p),
                 ("out_count", C.c_void_p), ("workspace", C.c_void_p),
                 ("workspace_bytes", C.c_size_t), ("keys", KvView), ("rope", RopeCtx),
-                ("keys_exact", C.c_void_p)]
+                ("keys_exact", C.c_void_p), ("list_out", C.c_void_p),
+                ("list_out_stride", C.c_int64)]
 
 
 class DecodeBsaArgs(C.Structure):

@@ -118,6 +118,26 @@ __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
 
+// ---- last-CTA ticket ---------------------------------------------------------------
+// Called by all threads after the CTA's global writes. One thread takes the ticket
+// with a gpu-scope acq_rel atomic: release publishes every write the CTA made
+// before the barrier (PTX memory-model cumulativity through bar.sync), acquire
+// orders the last CTA's later reads after all other CTAs' writes. One fence per
+// CTA instead of a MEMBAR.GPU (+ L1 invalidate) in every thread. The last CTA
+// resets the counter for the next launch / graph replay.
+__device__ __forceinline__ bool cta_ticket_last(int* counter, int total, int* sh_flag) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int prev;
+        asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(prev) : "l"(counter) : "memory");
+        const bool last = prev == total - 1;
+        if (last) *counter = 0;
+        *sh_flag = last;
+    }
+    __syncthreads();
+    return *sh_flag != 0;
+}
+
 // ---- phase tracer (off unless hp_trace_enable set a buffer) ------------------------
 // Per-CTA %globaltimer stamps at named checkpoints of one kernel id, 8 slots per CTA.
 // internal linkage: each translation unit that traces exports its own enable call
@@ -133,6 +153,7 @@ __device__ __forceinline__ void trace(int kernel_id, int slot) {
     if (b != nullptr && g_trace_kernel == kernel_id && threadIdx.x == 0) {
         const unsigned cta = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
         b[cta * 8 + slot] = globaltimer();
+        b[(8192 + cta) * 8 + slot] = clock64();  // SM cycles at the same point
     }
 }
 

@@ -224,7 +224,7 @@ __device__ __forceinline__ int block_scan_rt(int v, int* tmp) {
 // on order keys (-0 folded onto +0), ties to the lowest chunk index, survivors
 // emitted in ascending chunk order (pruning.cpp:187-192).
 __device__ void cta_topk(const float* sc, int64_t cc, int K, int32_t* sel_out, uint32_t* skeys,
-                         int smem_cap) {
+                         int smem_cap, int trace_id) {
     __shared__ int hist[256];
     __shared__ int scan_tmp[32];
     __shared__ int sh_digit, sh_above;
@@ -250,6 +250,7 @@ __device__ void cta_topk(const float* sc, int64_t cc, int K, int32_t* sel_out, u
     // Radix select on v = key - kmin: chunk scores of one mask span a narrow range, so
     // digits start at the highest bit that differs and the bins spread out (plain
     // shared atomics, no same-address serialisation). Order is unchanged by the shift.
+    trace(trace_id, 6);
     __shared__ uint32_t sh_min, sh_max;
     uint32_t lmin = 0xffffffffu, lmax = 0u;
     for (int64_t j = threadIdx.x; j < cc; j += nt) {
@@ -265,45 +266,55 @@ __device__ void cta_topk(const float* sc, int64_t cc, int K, int32_t* sel_out, u
     __syncthreads();
     const uint32_t kmin = sh_min, range = sh_max - sh_min;
     auto key = [&](int64_t j) -> uint32_t { return (in_smem ? skeys[j] : order_key(__ldcg(sc + j))) - kmin; };
+    // 4-bit digits counted with warp ballots: each element contributes 5 ballots
+    // (validity + 4 digit bit-planes) and lane b < 16 popcounts bin b's mask. Shared
+    // atomics cost ~2 cycles per lane on this part; the ballot histogram has no
+    // contention and no atomics at all.
+    int* whist = hist;  // [nwarp (<= 16)][16] per-warp bin counts
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarp = nt >> 5;
     uint32_t prefix = 0, pmask = 0;
     int need = K;
     const int hb = range ? 31 - __clz(range) : 0;  // highest differing bit
-    for (int shift = hb >= 7 ? hb - 7 : 0;; shift -= 8) {
-        const int s = shift < 0 ? 0 : shift;
-        const int nbits = shift < 0 ? 8 + shift : 8;
-        const uint32_t dmask = (1u << nbits) - 1u;
-        for (int i = threadIdx.x; i < 256; i += nt) hist[i] = 0;
-        __syncthreads();
-        for (int64_t j = threadIdx.x; j < cc; j += nt) {
-            const uint32_t u = key(j);
-            if ((u & pmask) == prefix) atomicAdd(&hist[(u >> s) & dmask], 1);
+    int s = hb >= 3 ? hb - 3 : 0;                  // digit = bits [s, s+3]
+    for (;;) {
+        int cnt = 0;
+        for (int64_t b0 = static_cast<int64_t>(wid) * 32; b0 < cc; b0 += nt) {
+            const int64_t j = b0 + lane;
+            const uint32_t u = j < cc ? key(j) : 0u;
+            const uint32_t dg = (u >> s) & 15u;
+            const unsigned vb = __ballot_sync(0xffffffffu, j < cc && (u & pmask) == prefix);
+            const unsigned p0 = __ballot_sync(0xffffffffu, dg & 1u);
+            const unsigned p1 = __ballot_sync(0xffffffffu, dg & 2u);
+            const unsigned p2 = __ballot_sync(0xffffffffu, dg & 4u);
+            const unsigned p3 = __ballot_sync(0xffffffffu, dg & 8u);
+            const unsigned m = vb & ((lane & 1) ? p0 : ~p0) & ((lane & 2) ? p1 : ~p1) &
+                               ((lane & 4) ? p2 : ~p2) & ((lane & 8) ? p3 : ~p3);
+            cnt += __popc(m);
         }
+        if (lane < 16) whist[wid * 16 + lane] = cnt;
         __syncthreads();
-        if (threadIdx.x < 32) {
-            const int lane = threadIdx.x;
-            int c[8], tot = 0;
+        if (wid == 0) {
+            int c = 0;
+            if (lane < 16)
+                for (int w2 = 0; w2 < nwarp; ++w2) c += whist[w2 * 16 + lane];
+            int suf = c;  // inclusive suffix over bins [lane, 15]
 #pragma unroll
-            for (int k = 0; k < 8; ++k) { c[k] = hist[lane * 8 + k]; tot += c[k]; }
-            int suf = tot;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
+            for (int o = 1; o < 16; o <<= 1) {
                 const int y = __shfl_down_sync(0xffffffffu, suf, o);
-                if (lane + o < 32) suf += y;
+                if (lane + o < 16) suf += y;
             }
-            int above = suf - tot;
-#pragma unroll
-            for (int k = 7; k >= 0; --k) {
-                if (above < need && need <= above + c[k]) { sh_digit = lane * 8 + k; sh_above = above; }
-                above += c[k];
-            }
+            const int above = suf - c;
+            const unsigned hit = __ballot_sync(0xffffffffu, lane < 16 && above < need && need <= above + c);
+            if (lane == __ffs(hit) - 1) { sh_digit = lane; sh_above = above; }
         }
         __syncthreads();
         prefix |= static_cast<uint32_t>(sh_digit) << s;
-        pmask |= dmask << s;
+        pmask |= 15u << s;
         need -= sh_above;
-        __syncthreads();
         if (s == 0) break;
+        s = s >= 4 ? s - 4 : 0;  // a final overlapping digit re-reads fixed bits: harmless
     }
+    trace(trace_id, 7);
     // Each thread owns a contiguous run of chunk indices so ranks follow index order.
     const int64_t per = (cc + nt - 1) / nt;
     const int64_t j0 = min64(cc, threadIdx.x * per), j1 = min64(cc, j0 + per);
@@ -326,10 +337,133 @@ __device__ void cta_topk(const float* sc, int64_t cc, int K, int32_t* sel_out, u
     __syncthreads();
 }
 
+// Histogram-guided exact top-K (the fast path). Every descent CTA has already added
+// its chunks' order keys to two global per-mask histograms — coarse (key >> 24) and
+// fine (key >> 16) — so the last CTA only walks two 256-bin slices to find the
+// 16-bit bin holding the K-th largest key, resolves that bin's few members exactly
+// by (key desc, chunk asc) rank, and compacts the survivors in chunk order. It
+// resets every bin it consumed for the next launch. Returns false (nothing written)
+// when the inputs do not fit its shared buffers; the caller then runs cta_topk.
+constexpr int kTopkSmemKeys = 4096;
+constexpr int kCandCap = 512;
+
+__device__ bool cta_topk_hist(const float* sc, int64_t cc, int K, int32_t* sel_out,
+                              unsigned char* buf, int* coarse, int* fine, int trace_id) {
+    __shared__ int scan_tmp[32];
+    __shared__ int sh_c, sh_above_c, sh_f, sh_above_f, sh_ncand;
+    if (cc > kTopkSmemKeys) return false;
+    const int nt = blockDim.x, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t* keys = reinterpret_cast<uint32_t*>(buf);                    // [cc]
+    uint32_t* cand_key = keys + kTopkSmemKeys;                             // [kCandCap]
+    int* cand_idx = reinterpret_cast<int*>(cand_key + kCandCap);           // [kCandCap]
+    uint32_t* selbits = reinterpret_cast<uint32_t*>(cand_idx + kCandCap);  // [kTopkSmemKeys/32]
+    int* h = reinterpret_cast<int*>(selbits + kTopkSmemKeys / 32);         // [256]
+    int* hc = h + 256;                                                     // [256] coarse copy
+    // batched key loads + coarse histogram fetch
+    for (int64_t b0 = 0; b0 < cc; b0 += 8 * nt) {
+        float v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int64_t j = b0 + k * nt + threadIdx.x;
+            v[k] = __ldcg(sc + min64(j, cc - 1));
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int64_t j = b0 + k * nt + threadIdx.x;
+            if (j < cc) keys[j] = order_key(v[k]);
+        }
+    }
+    for (int i = threadIdx.x; i < 256; i += nt) h[i] = hc[i] = __ldcg(coarse + i);
+    for (int i = threadIdx.x; i < kTopkSmemKeys / 32; i += nt) selbits[i] = 0u;
+    if (threadIdx.x == 0) sh_ncand = 0;
+    __syncthreads();
+    trace(trace_id, 6);
+    // one warp finds the bin holding the K-th largest from the top (8 bins per lane)
+    auto find_digit = [&](int need, int* out_digit, int* out_above) {
+        if (wid == 0) {
+            int c[8], tot = 0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) { c[k] = h[lane * 8 + k]; tot += c[k]; }
+            int suf = tot;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_down_sync(0xffffffffu, suf, o);
+                if (lane + o < 32) suf += y;
+            }
+            int above = suf - tot;
+#pragma unroll
+            for (int k = 7; k >= 0; --k) {
+                if (above < need && need <= above + c[k]) { *out_digit = lane * 8 + k; *out_above = above; }
+                above += c[k];
+            }
+        }
+        __syncthreads();
+    };
+    find_digit(K, &sh_c, &sh_above_c);
+    const int cstar = sh_c;
+    for (int i = threadIdx.x; i < 256; i += nt) h[i] = __ldcg(fine + cstar * 256 + i);
+    __syncthreads();
+    find_digit(K - sh_above_c, &sh_f, &sh_above_f);
+    const uint32_t t16 = (static_cast<uint32_t>(cstar) << 8) | static_cast<uint32_t>(sh_f);
+    const int need = K - sh_above_c - sh_above_f;  // members of bin t16 to keep (>= 1)
+    const int m = h[sh_f];
+    if (m > kCandCap) {
+        // pathological concentration: leave the histograms to be reset by the caller path
+        return false;
+    }
+    // gather the threshold bin's members
+    for (int64_t j = threadIdx.x; j < cc; j += nt) {
+        const uint32_t u = keys[j];
+        if ((u >> 16) == t16) {
+            const int p = atomicAdd(&sh_ncand, 1);
+            cand_key[p] = u;
+            cand_idx[p] = static_cast<int>(j);
+        }
+    }
+    __syncthreads();
+    // exact rank inside the bin: (key desc, chunk asc) == the reference's stable order
+    for (int i = threadIdx.x; i < m; i += nt) {
+        const uint32_t ki = cand_key[i];
+        const int ii = cand_idx[i];
+        int rank = 0;
+        for (int c = 0; c < m; ++c) {
+            const uint32_t kc = cand_key[c];
+            rank += kc > ki || (kc == ki && cand_idx[c] < ii);
+        }
+        if (rank < need) atomicOr(&selbits[ii >> 5], 1u << (ii & 31));
+    }
+    __syncthreads();
+    trace(trace_id, 7);
+    // ordered emission over contiguous per-thread runs; reset the consumed bins
+    const int64_t per = (cc + nt - 1) / nt;
+    const int64_t j0 = min64(cc, threadIdx.x * per), j1 = min64(cc, j0 + per);
+    int take = 0;
+    for (int64_t j = j0; j < j1; ++j) {
+        const uint32_t u16 = keys[j] >> 16;
+        take += u16 > t16 || (u16 == t16 && ((selbits[j >> 5] >> (j & 31)) & 1u));
+    }
+    // reset: every coarse bin, plus the fine slice under each occupied coarse bin
+    for (int b = threadIdx.x; b < 256; b += nt) {
+        if (hc[b] > 0) {
+            int4* f4 = reinterpret_cast<int4*>(fine + b * 256);
+            for (int i = 0; i < 64; ++i) f4[i] = make_int4(0, 0, 0, 0);
+        }
+        coarse[b] = 0;
+    }
+    int r = block_scan_rt(take, scan_tmp);
+    for (int64_t j = j0; j < j1; ++j) {
+        const uint32_t u16 = keys[j] >> 16;
+        if (u16 > t16 || (u16 == t16 && ((selbits[j >> 5] >> (j & 31)) & 1u))) sel_out[r++] = static_cast<int32_t>(j);
+    }
+    __syncthreads();
+    return true;
+}
+
 // ------------------------------------------------------------------ stage kernel
 template <typename T, bool EXT>
 __global__ void __launch_bounds__(kStageWarps * 32, 7)
-decode_stage_kernel(const hp_decode_stage_args a, float* scores, int* tickets, int cg, int prefetch) {
+decode_stage_kernel(const hp_decode_stage_args a, float* scores, int* tickets, int* hist_coarse,
+                    int* hist_fine, int cg, int prefetch) {
     extern __shared__ __align__(128) unsigned char smem[];
     using G = RowGeom<T>;
     const int hpm = a.heads_per_mask;
@@ -453,41 +587,211 @@ decode_stage_kernel(const hp_decode_stage_args a, float* scores, int* tickets, i
         __syncwarp();
     }
     __syncthreads();
-    for (int c = threadIdx.x; c < chunks_per_cta; c += blockDim.x) {
+    for (int c0 = 0; c0 < chunks_per_cta; c0 += blockDim.x) {  // warp-uniform trip count
+        const int c = c0 + threadIdx.x;
         const int64_t jj = chunk0 + c;
-        if (jj >= cc) continue;
+        const bool valid = c < chunks_per_cta && jj < cc;
         float best = -INFINITY;
-        for (int h = 0; h < hpm; ++h) {
-            const float s = red[h * chunks_per_cta + c];
-            best = (best < s) ? s : best;  // std::max (pruning.cpp:182)
+        if (valid) {
+            for (int h = 0; h < hpm; ++h) {
+                const float s = red[h * chunks_per_cta + c];
+                best = (best < s) ? s : best;  // std::max (pruning.cpp:182)
+            }
+            scores[static_cast<int64_t>(m) * a.max_chunks + jj] = best;
         }
-        scores[static_cast<int64_t>(m) * a.max_chunks + jj] = best;
+        // Feed the selection histograms. A mask's scores share one or two coarse bins,
+        // so same-bin lanes are merged first (one RED per distinct bin per warp) to
+        // keep thousands of same-address atomics off the L2 slice.
+        const uint32_t u = order_key(best);
+        const int cb = valid ? static_cast<int>(u >> 24) : -1;
+        const int fb = valid ? static_cast<int>(u >> 16) : -1;
+        const unsigned cpeers = __match_any_sync(0xffffffffu, cb);
+        const unsigned fpeers = __match_any_sync(0xffffffffu, fb);
+        const int lane = threadIdx.x & 31;
+        if (valid && lane == __ffs(cpeers) - 1) atomicAdd(hist_coarse + m * 256 + cb, __popc(cpeers));
+        if (valid && lane == __ffs(fpeers) - 1) atomicAdd(hist_fine + static_cast<int64_t>(m) * 65536 + fb, __popc(fpeers));
     }
     trace(10 + lc, 2);
-    // last CTA of this mask runs the selection
-    __shared__ int sh_last;
-    __threadfence();
+    (void)tickets;
+}
+
+// ----------------------------------------------------------------- top-k kernel
+// Exact top-(k/l_c) chunk selection for one mask by a 1024-thread CTA (32 warps:
+// every phase has enough warps to hide latency; a 4-warp "last CTA" did not).
+// The descent kernel already built the mask's coarse (key >> 24) and fine
+// (key >> 16) histograms, so: two 256-bin searches locate the 16-bit bin holding
+// the K-th largest order key, that bin's members are ranked exactly by
+// (key desc, chunk asc) — the reference's stable_sort order (pruning.cpp:187-192)
+// — and one block scan emits the kept chunk ids in ascending order. A radix
+// select over the keys covers the pathological case of a crowded bin.
+constexpr int kTopkThreads2 = 1024;
+constexpr int kTopkMaxKeys = 16384;
+
+__device__ __forceinline__ int block_scan_1024(int v, int* tmp) { return block_scan_rt(v, tmp); }
+
+// Finds bin b with above(b) < need <= above(b) + h[b], above(b) = sum_{b' > b} h[b'].
+// h: 256 shared counts; all threads call; result in *digit / *above.
+__device__ __forceinline__ void find_bin_256(const int* h, int need, int* tmp, int* digit, int* above) {
+    const int t = threadIdx.x;
+    const int c = t < 256 ? h[255 - t] : 0;  // reversed: bin 255 first
+    const int ex = block_scan_rt(c, tmp);     // count of bins above (255 - t)
+    if (t < 256 && ex < need && need <= ex + c) { *digit = 255 - t; *above = ex; }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        const int total = static_cast<int>((cc + chunks_per_cta - 1) / chunks_per_cta);
-        const int prev = atomicAdd(&tickets[m], 1);
-        sh_last = prev == total - 1;
-        if (sh_last) tickets[m] = 0;  // self-reset for the next launch / graph replay
-    }
-    __syncthreads();
-    trace(10 + lc, 3);
-    if (!sh_last) return;
-    trace(10 + lc, 4);
-    __threadfence();
-    const int smem_cap = static_cast<int>((static_cast<size_t>(nwarps) * 32 * G::bytes) / 4);
+}
+
+__global__ void __launch_bounds__(kTopkThreads2)
+decode_topk_kernel(const hp_decode_stage_args a, const float* scores, int* hist_coarse, int* hist_fine) {
+    extern __shared__ __align__(16) unsigned char tsm[];
+    __shared__ int scan_tmp[32];
+    __shared__ int sh_c, sh_ac, sh_f, sh_af, sh_ncand;
+    const int m = blockIdx.x, t = threadIdx.x, nt = blockDim.x;
+    const int n_in = a.in_count ? a.in_count[m] : static_cast<int>(a.in_count_const);
+    const int lc = a.chunk_size;
+    const int cc = (n_in + lc - 1) / lc;
+    const int K = a.keep / lc;
     int32_t* sel = a.sel_out + static_cast<int64_t>(m) * a.sel_stride;
-    cta_topk(scores + static_cast<int64_t>(m) * a.max_chunks, cc, K, sel,
-             reinterpret_cast<uint32_t*>(stage), smem_cap);
-    if (threadIdx.x == 0) {
-        const int64_t lastc = sel[K - 1];
-        a.out_count[m] = static_cast<int32_t>(static_cast<int64_t>(K - 1) * lc + min64(lc, n_in - lastc * lc));
+    if (n_in <= a.keep || cc <= K) {  // identity: every chunk kept (pruning.cpp:159-168)
+        for (int j = t; j < cc; j += nt) sel[j] = j;
+        if (t == 0) a.out_count[m] = n_in;
+        if (a.list_out)
+            for (int i = t; i < n_in; i += nt)
+                a.list_out[m * a.list_out_stride + i] = static_cast<int32_t>(ref_token(a.in, m, i));
+        return;
     }
-    trace(10 + lc, 5);
+    trace(3, 0);
+    const float* sc = scores + static_cast<int64_t>(m) * a.max_chunks;
+    int* co = hist_coarse + m * 256;
+    int* fi = hist_fine + static_cast<int64_t>(m) * 65536;
+    uint32_t* keys = reinterpret_cast<uint32_t*>(tsm);              // [cc]
+    uint32_t* selbits = keys + kTopkMaxKeys;                         // [kTopkMaxKeys / 32]
+    uint32_t* cand_key = selbits + kTopkMaxKeys / 32;                // [kCandCap]
+    int* cand_idx = reinterpret_cast<int*>(cand_key + kCandCap);     // [kCandCap]
+    int* h = cand_idx + kCandCap;                                    // [256]
+    int* hc = h + 256;                                               // [256]
+    constexpr int kPer = kTopkMaxKeys / kTopkThreads2;               // 16
+    {
+        float v[kPer];
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const int j = k * nt + t;
+            v[k] = j < cc ? __ldcg(sc + j) : 0.f;
+        }
+        if (t < 256) h[t] = hc[t] = __ldcg(co + t);
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const int j = k * nt + t;
+            if (j < cc) keys[j] = order_key(v[k]);
+        }
+        for (int i = t; i < (cc + 31) / 32; i += nt) selbits[i] = 0u;
+        if (t == 0) sh_ncand = 0;
+    }
+    __syncthreads();
+    trace(3, 1);
+    find_bin_256(h, K, scan_tmp, &sh_c, &sh_ac);
+    const int cstar = sh_c;
+    if (t < 256) h[t] = __ldcg(fi + cstar * 256 + t);
+    __syncthreads();
+    find_bin_256(h, K - sh_ac, scan_tmp, &sh_f, &sh_af);
+    const uint32_t t16 = (static_cast<uint32_t>(cstar) << 8) | static_cast<uint32_t>(sh_f);
+    const int need = K - sh_ac - sh_af;  // members of bin t16 to keep (>= 1)
+    const int mc = h[sh_f];
+    trace(3, 2);
+    if (mc <= kCandCap) {
+        for (int j = t; j < cc; j += nt) {
+            const uint32_t u = keys[j];
+            if ((u >> 16) == t16) {
+                const int p = atomicAdd(&sh_ncand, 1);
+                cand_key[p] = u;
+                cand_idx[p] = j;
+            }
+        }
+        __syncthreads();
+        for (int i = t; i < mc; i += nt) {
+            const uint32_t ki = cand_key[i];
+            const int ii = cand_idx[i];
+            int rank = 0;
+            for (int c = 0; c < mc; ++c) {
+                const uint32_t kc = cand_key[c];
+                rank += kc > ki || (kc == ki && cand_idx[c] < ii);
+            }
+            if (rank < need) atomicOr(&selbits[ii >> 5], 1u << (ii & 31));
+        }
+    } else {
+        // crowded threshold bin: exact 4-bit ballot radix select among its members
+        // (low 16 bits), then mark the first `need` of the chosen key by chunk order
+        uint32_t prefix = 0, pmask = 0;
+        int nd = need;
+        for (int s = 12;; s -= 4) {
+            int cnt = 0;
+            const int lane = t & 31, wid = t >> 5;
+            for (int b0 = wid * 32; b0 < cc; b0 += nt) {
+                const int j = b0 + lane;
+                const uint32_t u = j < cc ? keys[j] : 0u;
+                const bool in = j < cc && (u >> 16) == t16 && ((u & 0xffffu) & pmask) == prefix;
+                const uint32_t dg = (u >> s) & 15u;
+                const unsigned vb = __ballot_sync(0xffffffffu, in);
+                const unsigned p0 = __ballot_sync(0xffffffffu, dg & 1u), p1 = __ballot_sync(0xffffffffu, dg & 2u);
+                const unsigned p2 = __ballot_sync(0xffffffffu, dg & 4u), p3 = __ballot_sync(0xffffffffu, dg & 8u);
+                cnt += __popc(vb & ((lane & 1) ? p0 : ~p0) & ((lane & 2) ? p1 : ~p1) &
+                              ((lane & 4) ? p2 : ~p2) & ((lane & 8) ? p3 : ~p3));
+            }
+            if (t < 256) h[t] = 0;
+            __syncthreads();
+            if (lane < 16 && cnt) atomicAdd(&h[lane], cnt);
+            __syncthreads();
+            find_bin_256(h, nd, scan_tmp, &sh_f, &sh_af);  // bins 16..255 are empty
+            prefix |= static_cast<uint32_t>(sh_f) << s;
+            pmask |= 15u << s;
+            nd -= sh_af;
+            if (s == 0) break;
+        }
+        // keys equal to (t16, prefix): keep the first nd by chunk index; greater keys all kept
+        const uint32_t kth = (t16 << 16) | prefix;
+        const int per = (cc + nt - 1) / nt;
+        const int j0 = min(cc, t * per), j1 = min(cc, j0 + per);
+        int eq = 0;
+        for (int j = j0; j < j1; ++j) eq += keys[j] == kth;
+        int r = block_scan_rt(eq, scan_tmp);
+        for (int j = j0; j < j1; ++j) {
+            const uint32_t u = keys[j];
+            if ((u >> 16) == t16 && (u > kth || (u == kth && r++ < nd))) atomicOr(&selbits[j >> 5], 1u << (j & 31));
+        }
+    }
+    __syncthreads();
+    trace(3, 3);
+    // ordered emission over contiguous per-thread runs
+    const int per = (cc + nt - 1) / nt;
+    const int j0 = min(cc, t * per), j1 = min(cc, j0 + per);
+    int take = 0;
+    for (int j = j0; j < j1; ++j) {
+        const uint32_t u16 = keys[j] >> 16;
+        take += u16 > t16 || (u16 == t16 && ((selbits[j >> 5] >> (j & 31)) & 1u));
+    }
+    int r = block_scan_rt(take, scan_tmp);
+    for (int j = j0; j < j1; ++j) {
+        const uint32_t u16 = keys[j] >> 16;
+        if (u16 > t16 || (u16 == t16 && ((selbits[j >> 5] >> (j & 31)) & 1u))) sel[r++] = j;
+    }
+    // reset the histograms for the next stage / launch
+    if (t < 256) {
+        if (hc[t] > 0) {
+            int4* f4 = reinterpret_cast<int4*>(fi + t * 256);
+            for (int i = 0; i < 64; ++i) f4[i] = make_int4(0, 0, 0, 0);
+        }
+        co[t] = 0;
+    }
+    __syncthreads();
+    const int lastc = sel[K - 1];
+    const int n_out = (K - 1) * lc + min(lc, n_in - lastc * lc);
+    if (t == 0) a.out_count[m] = n_out;
+    if (a.list_out) {  // materialize: output position o -> chunk sel[o / lc] -> input list
+        for (int o = t; o < n_out; o += nt) {
+            const int r = o / lc;
+            a.list_out[m * a.list_out_stride + o] =
+                static_cast<int32_t>(ref_token(a.in, m, static_cast<int64_t>(sel[r]) * lc + (o - r * lc)));
+        }
+    }
+    trace(3, 4);
 }
 
 // -------------------------------------------------------------------- BSA kernel
@@ -643,18 +947,10 @@ decode_bsa_kernel(const hp_decode_bsa_args a, float* part, int* tickets, int spl
         if (e == 0) { pp[0] = M; pp[1] = L; }
         pp[2 + e] = o;
     }
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const int prev = atomicAdd(&tickets[hg], 1);
-        sh_last = prev == splits - 1;
-        if (sh_last) tickets[hg] = 0;
-    }
-    __syncthreads();
+    const bool last_cta = cta_ticket_last(&tickets[hg], splits, &sh_last);
     trace(2, 6);
-    if (!sh_last) return;
+    if (!last_cta) return;
     trace(2, 3);
-    __threadfence();
     // Merge all splits of this head group (log-sum-exp). Phase 1 pulls every (m, l)
     // in one parallel load, phase 2 forms per-split weights, phase 3 streams the o's
     // with independent (pipelined) loads.
@@ -663,6 +959,7 @@ decode_bsa_kernel(const hp_decode_bsa_args a, float* part, int* tickets, int spl
     float* ml = wgt + kMaxSplitsSmem * HC;        // [splits][HC][2]
     const bool fits = splits <= kMaxSplitsSmem && 3 * kMaxSplitsSmem * HC <= kBsaWarps * HC * kD;
     const float* pbase = part + static_cast<int64_t>(hg) * splits * HC * (kD + 2);
+    trace(2, 7);
     if (fits) {
         for (int i = threadIdx.x; i < splits * HC; i += blockDim.x) {
             const float* pp = pbase + static_cast<int64_t>(i) * (kD + 2);
@@ -689,6 +986,7 @@ decode_bsa_kernel(const hp_decode_bsa_args a, float* part, int* tickets, int spl
         }
         __syncthreads();
     }
+    trace(2, 5);
     for (int idx = threadIdx.x; idx < HC * kD; idx += blockDim.x) {
         const int hh = idx / kD, e = idx - hh * kD;
         const float* pb = pbase + static_cast<int64_t>(hh) * (kD + 2);
@@ -698,16 +996,18 @@ decode_bsa_kernel(const hp_decode_bsa_args a, float* part, int* tickets, int spl
             L = sm_l[0][hh];
             constexpr int kBatch = 16;  // independent loads in flight per thread
             for (int s0 = 0; s0 < splits; s0 += kBatch) {
+                // unconditional loads (clamped index, zero weight past the end) so the
+                // batch issues back to back instead of load->use->load on one register
                 float vals[kBatch];
 #pragma unroll
                 for (int k = 0; k < kBatch; ++k) {
-                    const int s = s0 + k;
-                    vals[k] = s < splits ? __ldcg(pb + static_cast<int64_t>(s) * HC * (kD + 2) + 2 + e) : 0.f;
+                    const int s = min(s0 + k, splits - 1);
+                    vals[k] = __ldcg(pb + static_cast<int64_t>(s) * HC * (kD + 2) + 2 + e);
                 }
 #pragma unroll
                 for (int k = 0; k < kBatch; ++k) {
                     const int s = s0 + k;
-                    if (s < splits) o += vals[k] * wgt[s * HC + hh];
+                    o += vals[k] * (s < splits ? wgt[min(s, splits - 1) * HC + hh] : 0.f);
                 }
             }
         } else {
@@ -761,7 +1061,8 @@ int bsa_hc(int n_q_heads, int n_kv, int hpm) {
 }
 
 template <typename T, bool EXT>
-cudaError_t launch_stage(const hp_decode_stage_args& a, float* scores, int* tickets, cudaStream_t s) {
+cudaError_t launch_stage(const hp_decode_stage_args& a, float* scores, int* tickets, int* coarse,
+                         int* fine, cudaStream_t s) {
     using G = RowGeom<T>;
     const int hpm = a.heads_per_mask;
     int cg = std::max(1, kStageWarps / hpm);
@@ -777,7 +1078,12 @@ cudaError_t launch_stage(const hp_decode_stage_args& a, float* scores, int* tick
     // speculative next-row prefetch only where the stage is latency-bound (few descents)
     const int64_t lanes = static_cast<int64_t>(a.n_masks) * a.max_chunks * hpm;
     const int prefetch = lanes <= 65536 ? 1 : 0;
-    kern<<<grid, threads, smem, s>>>(a, scores, tickets, cg, prefetch);
+    kern<<<grid, threads, smem, s>>>(a, scores, tickets, coarse, fine, cg, prefetch);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    const size_t tsmem = static_cast<size_t>(kTopkMaxKeys) * 4 + kTopkMaxKeys / 8 + kCandCap * 8 + 512 * 4;
+    e = cudaFuncSetAttribute(decode_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(tsmem));
+    if (e != cudaSuccess) return e;
+    decode_topk_kernel<<<a.n_masks, kTopkThreads2, tsmem, s>>>(a, scores, coarse, fine);
     return cudaGetLastError();
 }
 
@@ -808,8 +1114,10 @@ extern "C" int hp_trace_enable(unsigned long long* buf, int kernel_id) {
 }
 
 extern "C" size_t hp_decode_stage_workspace_bytes(int32_t n_masks, int32_t max_chunks) {
-    return align_up(static_cast<size_t>(n_masks) * std::max(1, max_chunks) * 4, 256) +
-           align_up(static_cast<size_t>(n_masks) * 4, 256);
+    return align_up(static_cast<size_t>(n_masks) * 4, 256) +             // tickets
+           align_up(static_cast<size_t>(n_masks) * 256 * 4, 256) +       // coarse histograms
+           static_cast<size_t>(n_masks) * 65536 * 4 +                     // fine histograms
+           align_up(static_cast<size_t>(n_masks) * std::max(1, max_chunks) * 4, 256);  // scores
 }
 
 extern "C" int hp_decode_stage(const hp_decode_stage_args* ap, void* stream) {
@@ -824,6 +1132,9 @@ extern "C" int hp_decode_stage(const hp_decode_stage_args* ap, void* stream) {
     if (a.in.depth < 0 || a.in.depth > 4) return hph::set_error(HP_INVALID_ARGUMENT, "hp_decode_stage: list depth");
     if (a.sel_stride < a.keep / a.chunk_size) return hph::set_error(HP_INVALID_ARGUMENT, "hp_decode_stage: sel_stride < k/l_c");
     if (a.max_chunks <= 0) return hph::set_error(HP_INVALID_ARGUMENT, "hp_decode_stage: max_chunks must be >= 1");
+    if (a.max_chunks > kTopkMaxKeys)
+        return hph::set_error(HP_INVALID_ARGUMENT, "hp_decode_stage: %d chunks per list exceed the fused selection limit %d",
+                              a.max_chunks, kTopkMaxKeys);
     const size_t need = hp_decode_stage_workspace_bytes(a.n_masks, a.max_chunks);
     if (!a.workspace || a.workspace_bytes < need) return hph::set_error(HP_INVALID_ARGUMENT, "hp_decode_stage: workspace too small");
     if (a.rope.extension) {
@@ -836,16 +1147,21 @@ extern "C" int hp_decode_stage(const hp_decode_stage_args* ap, void* stream) {
             return hph::set_error(HP_OUT_OF_RANGE, "apply_rope: position %lld >= max_position %lld",
                                   static_cast<long long>(std::max(need_q, need_k)), static_cast<long long>(a.rope.rope_max));
     }
+    // Fixed-offset regions first (tickets, selection histograms): they must stay zero
+    // between launches and every stage shares this workspace; scores last (size varies).
     char* ws = static_cast<char*>(a.workspace);
-    // tickets first: a fixed offset for every stage sharing this workspace (they must
-    // stay zero between launches; the scores region size varies per stage)
     int* tickets = reinterpret_cast<int*>(ws);
-    float* scores = reinterpret_cast<float*>(ws + align_up(static_cast<size_t>(a.n_masks) * 4, 256));
+    size_t off = align_up(static_cast<size_t>(a.n_masks) * 4, 256);
+    int* coarse = reinterpret_cast<int*>(ws + off);
+    off += align_up(static_cast<size_t>(a.n_masks) * 256 * 4, 256);
+    int* fine = reinterpret_cast<int*>(ws + off);
+    off += static_cast<size_t>(a.n_masks) * 65536 * 4;
+    float* scores = reinterpret_cast<float*>(ws + off);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const bool ext = a.rope.extension != 0;
     cudaError_t e;
-    if (a.keys.dtype == HP_BF16) e = ext ? launch_stage<bf16_t, true>(a, scores, tickets, s) : launch_stage<bf16_t, false>(a, scores, tickets, s);
-    else e = ext ? launch_stage<float, true>(a, scores, tickets, s) : launch_stage<float, false>(a, scores, tickets, s);
+    if (a.keys.dtype == HP_BF16) e = ext ? launch_stage<bf16_t, true>(a, scores, tickets, coarse, fine, s) : launch_stage<bf16_t, false>(a, scores, tickets, coarse, fine, s);
+    else e = ext ? launch_stage<float, true>(a, scores, tickets, coarse, fine, s) : launch_stage<float, false>(a, scores, tickets, coarse, fine, s);
     return hph::check_cuda(e, "decode_stage_kernel");
 }
 

@@ -481,9 +481,13 @@ class FusedDecodeLayer:
                     sel_out=_ptr(self.sel[i]), out_count=_ptr(self.count[i]),
                     workspace=_ptr(self.ws_stage), workspace_bytes=self.ws_stage.numel(),
                     keys=kvv, rope=self.policy.ctx(self.layer1, self.rope),
-                    keys_exact=_ptr(self.kv.keys_exact))
+                    keys_exact=_ptr(self.kv.keys_exact),
+                    # the last stage materializes its list (= its cache) for the BSA
+                    list_out=_ptr(self.cache[i]) if i == S - 1 else None,
+                    list_out_stride=self.cache[i].shape[-1])
                 check(lib().hp_decode_stage(C.byref(a), sp))
-                chains[i] = _ref_push(in_ref, self.sel[i], lc)
+                chains[i] = (_ref_list(self.cache[i]) if i == S - 1
+                             else _ref_push(in_ref, self.sel[i], lc))
             else:
                 chains[i] = _ref_list(self.cache[i])
         b = _capi.DecodeBsaArgs(
@@ -495,7 +499,7 @@ class FusedDecodeLayer:
             rope=self.policy.ctx(0, self.rope))
         check(lib().hp_decode_bsa(C.byref(b), sp))
         if materialize:
-            idx = [i for i in range(S) if refresh[i]]
+            idx = [i for i in range(S - 1) if refresh[i]]  # the last stage wrote its own
             if idx:
                 n = len(idx)
                 refs = (_capi.ListRef * n)(*[chains[i] for i in idx])

@@ -18,12 +18,12 @@ layer = D.FusedDecodeLayer(kv, stages, sink=256, stream_tokens=1024, n_q_heads=g
 layer.q.copy_(q.view(layer.q.shape))
 L = _capi.lib()
 L.hp_trace_enable.argtypes = [C.c_void_p, C.c_int]
-buf = torch.zeros((8192, 8), dtype=torch.int64, device="cuda")
+buf = torch.zeros((16384, 8), dtype=torch.int64, device="cuda")
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 for _ in range(3):
     layer.run(t)
 torch.cuda.synchronize()
-names = {10 + 256: "stage1", 10 + 32: "stage2", 10 + 8: "stage3", 2: "bsa"}
+names = {10 + 256: "stage1", 10 + 32: "stage2", 10 + 8: "stage3", 3: "topk(last stage)", 2: "bsa"}
 for kid, name in names.items():
     buf.zero_()
     _capi.check(L.hp_trace_enable(buf.data_ptr(), kid))
@@ -32,9 +32,20 @@ for kid, name in names.items():
     layer.run(t)
     torch.cuda.synchronize()
     _capi.check(L.hp_trace_enable(None, -1))
-    b = buf.cpu().numpy().astype(np.float64)
+    ball = buf.cpu().numpy().astype(np.float64)
+    b = ball[:8192]
+    clk = ball[8192:]
     used = b[:, 0] > 0
     b = b[used]
+    clk = clk[used]
+    last = b[:, 5] > 0
+    if last.any():
+        dt = b[last][:, 5] - b[last][:, 4]
+        dc = clk[last][:, 5] - clk[last][:, 4]
+        print(f"  last-CTA tail: {dt.mean()/1000:.2f} us, {dc.mean():.0f} cycles -> {dc.mean()/dt.mean():.3f} GHz")
+    dt = b[:, 2] - b[:, 0]
+    dc = clk[:, 2] - clk[:, 0]
+    print(f"  body: {dt.mean()/1000:.2f} us, {dc.mean():.0f} cycles -> {dc.mean()/dt.mean():.3f} GHz")
     t0 = b[:, 0].min()
     rel = np.where(b > 0, (b - t0) / 1000.0, np.nan)  # us
     print(f"== {name}: {used.sum()} CTAs traced")
