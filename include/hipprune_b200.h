@@ -66,6 +66,10 @@ typedef struct hp_kv_view {
     int32_t d;
     int32_t dtype;               /* hp_dtype */
     int32_t t_kv;                /* valid tokens (bounds) */
+    /* optional instrumentation: bit (kv * row_bits_stride + token) is set for every
+     * key row read (distinct-row / algorithmic-byte accounting; NULL = off) */
+    uint32_t* row_bits;
+    int64_t row_bits_stride;
 } hp_kv_view;
 
 /* RoPE context (StageContext, pruning.hpp:55-63 + RopePolicySet, rope_policy.hpp:24-34).
@@ -246,6 +250,12 @@ typedef struct hp_decode_bsa_args {
 
 size_t hp_decode_bsa_workspace_bytes(int32_t n_q_heads, int32_t max_sel);
 int hp_decode_bsa(const hp_decode_bsa_args* args, void* stream);
+
+/* Append one token's K/V rows (DecodeEngine::step, decode.cpp:202-208): rows
+ * [n_kv][d] (same dtype as the pools) land at `token` of the paged pools; keys_exact
+ * (optional device int) is cleared if a new key breaks the exact-product range. */
+int hp_decode_append(const hp_kv_view* kv, const void* k_rows, const void* v_rows, int64_t token,
+                     int32_t* keys_exact, void* stream);
 
 /* Expand lists: out[m][i] = ref(m, i) for i < count[m] (n_lists refs at once). */
 int hp_decode_materialize(const hp_list_ref* refs, const int32_t* const* counts,

@@ -38,7 +38,8 @@ class KvView(C.Structure):
     _fields_ = [("k_pool", C.c_void_p), ("v_pool", C.c_void_p), ("k_host", C.c_void_p),
                 ("v_host", C.c_void_p), ("page_table", C.c_void_p), ("touched", C.c_void_p),
                 ("num_pages", C.c_int32), ("page_size", C.c_int32), ("n_kv", C.c_int32),
-                ("d", C.c_int32), ("dtype", C.c_int32), ("t_kv", C.c_int32)]
+                ("d", C.c_int32), ("dtype", C.c_int32), ("t_kv", C.c_int32),
+                ("row_bits", C.c_void_p), ("row_bits_stride", C.c_int64)]
 
 
 class RopeCtx(C.Structure):
@@ -102,7 +103,7 @@ EXPORTS = ["hp_last_error", "hp_version", "hp_device_available", "hp_build_rope_
            "hp_stage_workspace_bytes", "hp_prune_stage", "hp_remap_blocks",
            "hp_selected_indices", "hp_bsa_workspace_bytes", "hp_bsa", "hp_lse_merge",
            "hp_decode_stage_workspace_bytes", "hp_decode_stage", "hp_decode_bsa_workspace_bytes",
-           "hp_decode_bsa", "hp_decode_materialize"]
+           "hp_decode_bsa", "hp_decode_materialize", "hp_decode_append"]
 
 
 def lib():
@@ -147,6 +148,9 @@ def lib():
     L.hp_decode_materialize.argtypes = [C.POINTER(ListRef), C.POINTER(C.c_void_p),
                                         C.POINTER(C.c_void_p), C.POINTER(C.c_int64), C.c_int32,
                                         C.c_int32, C.c_int32, C.c_void_p]
+    L.hp_decode_append.restype = C.c_int
+    L.hp_decode_append.argtypes = [C.POINTER(KvView), C.c_void_p, C.c_void_p, C.c_int64,
+                                   C.c_void_p, C.c_void_p]
     L.hp_lse_merge.restype = C.c_int
     L.hp_lse_merge.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
                                C.c_int32, C.c_void_p, C.c_void_p]

@@ -43,6 +43,10 @@ __device__ __forceinline__ const char* kv_row_ptr(const hp_kv_view& v, const voi
     const int64_t off = t32 - static_cast<uint32_t>(page) * ps;
     int64_t slot = v.page_table ? static_cast<int64_t>(v.page_table[page]) : page;
     const bool hit = slot >= 0;
+    if (v.row_bits != nullptr && pool == v.k_pool) {
+        const int64_t bit = kv * v.row_bits_stride + tok;
+        atomicOr(v.row_bits + (bit >> 5), 1u << (bit & 31));
+    }
     if (v.touched) {
         const uint8_t flag = hit ? 1 : 2;
         if (v.touched[page] != flag) v.touched[page] = flag;

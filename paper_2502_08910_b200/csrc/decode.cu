@@ -1202,6 +1202,40 @@ extern "C" int hp_decode_bsa(const hp_decode_bsa_args* ap, void* stream) {
     return hph::check_cuda(e, "decode_bsa_kernel");
 }
 
+__global__ void append_kernel(const hp_kv_view kv, const unsigned char* k_rows,
+                              const unsigned char* v_rows, int64_t token, int32_t* keys_exact) {
+    const int eb = kv.dtype == HP_BF16 ? 2 : 4;
+    const int row_bytes = kv.d * eb;
+    const int h = blockIdx.x;
+    char* kd = const_cast<char*>(kv_row_ptr(kv, kv.k_pool, kv.k_host, h, token, eb));
+    char* vd = kv.v_pool ? const_cast<char*>(kv_row_ptr(kv, kv.v_pool, kv.v_host, h, token, eb)) : nullptr;
+    bool ok = true;
+    for (int i = threadIdx.x; i < row_bytes; i += blockDim.x) {
+        kd[i] = k_rows[h * row_bytes + i];
+        if (vd) vd[i] = v_rows[h * row_bytes + i];
+    }
+    if (eb == 2) {
+        for (int i = threadIdx.x; i < kv.d; i += blockDim.x) {
+            const uint16_t bits = reinterpret_cast<const uint16_t*>(k_rows + h * row_bytes)[i];
+            const float x = fabsf(__uint_as_float(static_cast<uint32_t>(bits) << 16));
+            ok &= x == 0.0f || (x >= 1.0842022e-19f && x <= 9.2233720e18f);
+        }
+    } else {
+        ok = false;
+    }
+    if (!__syncthreads_and(ok) && threadIdx.x == 0 && keys_exact) atomicAnd(keys_exact, 0);
+}
+
+extern "C" int hp_decode_append(const hp_kv_view* kv, const void* k_rows, const void* v_rows,
+                                int64_t token, int32_t* keys_exact, void* stream) {
+    if (!kv || !k_rows) return hph::set_error(HP_INVALID_ARGUMENT, "hp_decode_append: null pointer");
+    if (token < 0 || token >= static_cast<int64_t>(kv->num_pages) * kv->page_size)
+        return hph::set_error(HP_OUT_OF_RANGE, "hp_decode_append: token beyond the cache capacity");
+    append_kernel<<<kv->n_kv, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+        *kv, static_cast<const unsigned char*>(k_rows), static_cast<const unsigned char*>(v_rows), token, keys_exact);
+    return hph::check_cuda(cudaGetLastError(), "append_kernel");
+}
+
 extern "C" int hp_decode_materialize(const hp_list_ref* refs, const int32_t* const* counts,
                                      int32_t* const* outs, const int64_t* out_strides,
                                      int32_t n_lists, int32_t n_masks, int32_t max_count,

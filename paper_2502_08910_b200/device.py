@@ -71,6 +71,7 @@ class PagedKV:
         self.v_pool = self._pack(v, device) if v is not None else None
         self.page_table = None
         self.touched = None
+        self.row_bits = None
         # device flag: every key is bf16 with |k| in [2^-63, 2^63] or 0, so bf16 q*k
         # products are exact in fp32 (lets the fused stage issue FFMA, see decode.cu)
         self.keys_exact = torch.zeros(1, dtype=torch.int32, device=device)
@@ -114,7 +115,27 @@ class PagedKV:
         return KvView(k_pool=_ptr(self.k_pool), v_pool=_ptr(self.v_pool), k_host=None,
                       v_host=None, page_table=_ptr(self.page_table), touched=_ptr(self.touched),
                       num_pages=self.num_pages, page_size=self.page_size, n_kv=self.n_kv,
-                      d=self.d, dtype=_DT[self.dtype], t_kv=t_kv if t_kv is not None else self.t_kv)
+                      d=self.d, dtype=_DT[self.dtype], t_kv=t_kv if t_kv is not None else self.t_kv,
+                      row_bits=_ptr(self.row_bits),
+                      row_bits_stride=self.num_pages * self.page_size)
+
+    def count_rows(self, enable: bool = True) -> None:
+        """Instrumentation: record every distinct key row read (see hp_kv_view.row_bits)."""
+        if enable:
+            nbits = self.n_kv * self.num_pages * self.page_size
+            self.row_bits = torch.zeros((nbits + 31) // 32, dtype=torch.int32, device=self.k_pool.device)
+        else:
+            self.row_bits = None
+
+    def distinct_rows(self) -> int:
+        b = self.row_bits
+        if b is None:
+            return 0
+        x = b.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+        cnt = torch.zeros_like(x)
+        for s in range(32):
+            cnt += (x >> s) & 1
+        return int(cnt.sum())
 
 
 # --------------------------------------------------------------------------- RoPE
@@ -509,6 +530,79 @@ class FusedDecodeLayer:
                 check(lib().hp_decode_materialize(refs, counts, outs, strides, n, self.n_masks,
                                                   max(self.stages[i][2] for i in idx), sp))
         return self.out
+
+    def run_stage(self, t: int, i: int = 0, stream=None) -> None:
+        """Launch only stage i (descent + selection) on its input: stage 0 reads the
+        range [n_sink, T - n_stream), later stages the materialized cache of i-1.
+        Used to time / instrument the dominant kernel in isolation."""
+        (_, lc, keep) = self.stages[i]
+        pos = t - 1
+        upper = t - self.stream_tokens if t > self.stream_tokens else 0
+        if i == 0:
+            in_ref, in_count, const = _ref_range(self.sink), None, max(0, upper - self.sink)
+        else:
+            in_ref, in_count, const = _ref_list(self.cache[i - 1]), self.count[i - 1], 0
+        a = _capi.DecodeStageArgs(
+            chunk_size=lc, keep=keep, n_masks=self.n_masks, heads_per_mask=self.hpm,
+            n_q_heads=self.n_q_heads, stream_tokens=self.stream_tokens, q=_ptr(self.q),
+            query_position=pos, in_=in_ref, in_count=_ptr(in_count), in_count_const=const,
+            max_chunks=self.max_chunks[i], sel_stride=self.sel[i].shape[-1],
+            sel_out=_ptr(self.sel[i]), out_count=_ptr(self.count[i]),
+            workspace=_ptr(self.ws_stage), workspace_bytes=self.ws_stage.numel(),
+            keys=self.kv.view(t), rope=self.policy.ctx(self.layer1, self.rope),
+            keys_exact=_ptr(self.kv.keys_exact), list_out=None, list_out_stride=0)
+        check(lib().hp_decode_stage(C.byref(a), C.c_void_p(_stream(stream))))
+
+    def step_host(self, t: int, q_host, k_row=None, v_row=None, out_host=None, refresh=None,
+                  sync: bool = True) -> torch.Tensor:
+        """The host-facing decode call for the token at position t-1 (what a serving
+        loop calls per layer): host q [n_q_heads, d] fp32 and the token's K/V rows
+        [n_kv, d] in, host output [n_q_heads, d] fp32 out. One CUDA graph per
+        (t, refresh): pinned H2D copy -> append kernel -> the layer step -> D2H copy.
+        Returns the pinned output buffer (valid after sync)."""
+        has_kv = k_row is not None
+        key = (t, tuple(refresh) if refresh is not None else None, has_kv)
+        if not hasattr(self, "_hg"):
+            dev = self.dev
+            self._hg = {}
+            self._h_q = torch.empty((self.n_q_heads, self.kv.d), dtype=torch.float32).pin_memory()
+            self._h_k = torch.empty((self.kv.n_kv, self.kv.d), dtype=self.kv.dtype).pin_memory()
+            self._h_v = torch.empty((self.kv.n_kv, self.kv.d), dtype=self.kv.dtype).pin_memory()
+            self._h_out = torch.empty((self.n_q_heads, self.kv.d), dtype=torch.float32).pin_memory()
+            self._d_k = torch.empty((self.kv.n_kv, self.kv.d), dtype=self.kv.dtype, device=dev)
+            self._d_v = torch.empty((self.kv.n_kv, self.kv.d), dtype=self.kv.dtype, device=dev)
+        self._h_q.copy_(torch.as_tensor(q_host).reshape(self._h_q.shape))
+        if has_kv:
+            self._h_k.copy_(torch.as_tensor(k_row).reshape(self._h_k.shape))
+            self._h_v.copy_(torch.as_tensor(v_row).reshape(self._h_v.shape))
+        g = self._hg.get(key)
+        if g is None:
+            def body():
+                self.q.copy_(self._h_q, non_blocking=True)
+                if has_kv:
+                    self._d_k.copy_(self._h_k, non_blocking=True)
+                    self._d_v.copy_(self._h_v, non_blocking=True)
+                    view = self.kv.view(t)
+                    check(lib().hp_decode_append(C.byref(view), _ptr(self._d_k), _ptr(self._d_v),
+                                                 t - 1, _ptr(self.kv.keys_exact),
+                                                 C.c_void_p(_stream())))
+                self.run(t, refresh=refresh)
+                self._h_out.copy_(self.out, non_blocking=True)
+            s = torch.cuda.Stream(device=self.dev)
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                body()  # warm-up outside capture
+            torch.cuda.current_stream().wait_stream(s)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                body()
+            self._hg[key] = g
+        g.replay()
+        if sync:
+            torch.cuda.current_stream().synchronize()
+            if out_host is not None:
+                torch.as_tensor(out_host).copy_(self._h_out.reshape(torch.as_tensor(out_host).shape))
+        return self._h_out
 
     def mask(self, stage: int = -1):
         """Materialized stage cache (lists, counts) — DecodeEngine::stage_cache."""
