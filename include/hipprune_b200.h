@@ -262,6 +262,11 @@ int hp_decode_materialize(const hp_list_ref* refs, const int32_t* const* counts,
                           int32_t* const* outs, const int64_t* out_strides, int32_t n_lists,
                           int32_t n_masks, int32_t max_count, void* stream);
 
+/* Developer instrumentation: per-CTA %globaltimer / clock64 stamps of the fused decode
+ * kernels (kernel_id 10 + l_c = stage descent, 3 = top-k, 2 = BSA) into
+ * buf [16384][8] u64 (first 8192 rows: timer, next 8192: clock). NULL disables. */
+int hp_trace_enable(unsigned long long* buf, int kernel_id);
+
 /* Log-sum-exp merge of per-shard (m, l, o) partials (C5 sequence sharding):
  * m, l [n_shards][n]; o [n_shards][n][d] -> out [n][d]. */
 int hp_lse_merge(const float* m, const float* l, const float* o, int32_t n_shards, int32_t n,

@@ -199,8 +199,8 @@ class Oracle:
 
     def select_rep(self, q, chunk, k, *, layer1=4, stream=0, qstart=0, ext=False, cutoff=3,
                    chunk_index=0, chunk_count=1, rope_max=0):
-        q = _f32(q); k = _f32(k); chunk = _i64(chunk) if len(chunk) else np.zeros(1, np.int64)
-        n = len(chunk) if chunk.size and len(chunk) else 0
+        n = len(chunk)
+        q = _f32(q); k = _f32(k); chunk = _i64(chunk) if n else np.zeros(1, np.int64)
         rows, d = q.shape
         t = k.shape[0]
         rep = C.c_int64(0)
