@@ -1,6 +1,8 @@
 """Quick per-phase timing of the decode layer step at C2/C3 shapes (dev tool).
 usage: quick_perf.py T [--ncu]"""
 import sys, time
+from pathlib import Path
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import torch
 from paper_2502_08910_b200 import device as D, synth
 
