@@ -11,7 +11,8 @@ import os
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "_lib" / "libhipprune_b200.so"
+LIB_PATH = PKG / "_lib" / ("libhipprune_b200_trace.so" if os.environ.get("HP_TRACE") == "1"
+                           else "libhipprune_b200.so")
 
 HP_OK = 0
 HP_F32, HP_BF16 = 0, 1

@@ -37,14 +37,15 @@ def _stale(target: Path, deps) -> bool:
 
 def build_cuda(force: bool = False, verbose: bool = False) -> Path:
     LIB.mkdir(exist_ok=True)
-    out = LIB / "libhipprune_b200.so"
+    traced = os.environ.get("HP_TRACE") == "1"  # dev build with the per-CTA phase tracer
+    out = LIB / ("libhipprune_b200_trace.so" if traced else "libhipprune_b200.so")
     deps = [CSRC / s for s in CUDA_SOURCES] + list(CSRC.glob("*.cuh")) + [ROOT / "include" / "hipprune_b200.h", Path(__file__)]
     if not force and not _stale(out, deps):
         return out
     objs, procs = [], []
     for src in CUDA_SOURCES:  # compile translation units in parallel
-        obj = LIB / (Path(src).stem + ".o")
-        cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-c", str(CSRC / src), "-o", str(obj)]
+        obj = LIB / (Path(src).stem + (".trace.o" if traced else ".o"))
+        cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *(["-DHP_TRACE"] if traced else []), "-c", str(CSRC / src), "-o", str(obj)]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         procs.append((src, subprocess.Popen(cmd)))

@@ -122,6 +122,47 @@ __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
 
+// ---- mbarrier + 1-D bulk copies (the TMA engine's non-tensor path) -------------------
+// A row gather is one cp.async.bulk per row (256 B bf16 / 512 B fp32): the copy engine
+// moves it global -> shared and signals completion as transaction bytes on an mbarrier,
+// so a CTA can put all of its rows in flight with one instruction each and a single wait.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(smem)),
+        "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// Row pointer plus residency (true = device slot; false = the mapped host tier, which
+// the bulk copy engine does not read: such rows are copied with plain loads).
+__device__ __forceinline__ bool kv_row_resident(const hp_kv_view& v, int64_t tok) {
+    if (!v.page_table) return true;
+    const uint32_t ps = static_cast<uint32_t>(v.page_size);
+    const uint32_t page = static_cast<uint32_t>(tok) / ps;
+    return v.page_table[page] >= 0;
+}
+
 // ---- last-CTA ticket ---------------------------------------------------------------
 // Called by all threads after the CTA's global writes. One thread takes the ticket
 // with a gpu-scope acq_rel atomic: release publishes every write the CTA made
@@ -152,7 +193,14 @@ __device__ __forceinline__ unsigned long long globaltimer() {
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
 }
+// Compiled in only with -DHP_TRACE (the dev build `HP_TRACE=1 python -m
+// paper_2502_08910_b200.build`): the enable check is a global load per call site.
 __device__ __forceinline__ void trace(int kernel_id, int slot) {
+#ifndef HP_TRACE
+    (void)kernel_id;
+    (void)slot;
+    return;
+#endif
     unsigned long long* b = g_trace_buf;
     if (b != nullptr && g_trace_kernel == kernel_id && threadIdx.x == 0) {
         const unsigned cta = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;

@@ -20,6 +20,13 @@ fused = "--generic" not in sys.argv
 layer = (D.FusedDecodeLayer if fused else D.DecodeLayer)(kv, stages, sink=256, stream_tokens=1024, n_q_heads=groups * hpm, n_masks=groups)
 layer.q.copy_(q.view(layer.q.shape))
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+flush_rd = torch.ones(512 << 20, dtype=torch.uint8, device="cuda")
+flush_out = torch.empty(1, dtype=torch.int64, device="cuda")
+def do_flush(mode):
+    if mode in ("w", "wr"):
+        flush.zero_()
+    if mode == "wr":  # evict the dirty lines: the timed step starts with a clean, cold L2
+        flush_out.copy_(flush_rd.view(torch.int64).sum().view(1))
 variants = {"full": [True] * 3, "s23_bsa": [False, True, True], "s3_bsa": [False, False, True],
             "bsa": [False] * 3}
 for _ in range(3):
@@ -42,15 +49,16 @@ for name, fl in variants.items():
         layer.run(t, refresh=fl)
     graphs[name] = g
 torch.cuda.synchronize()
-def timeit(g, n=20):
+def timeit(g, n=20, mode="w"):
     ts = []
     for _ in range(n):
-        flush.zero_()
+        do_flush(mode)
         a, b = torch.cuda.Event(True), torch.cuda.Event(True)
         a.record(); g.replay(); b.record(); torch.cuda.synchronize()
         ts.append(a.elapsed_time(b) * 1e3)
     ts.sort()
     return ts[len(ts) // 2]
-for name, g in graphs.items():
-    print(f"{name:10s} graph us (median, L2 flushed): {timeit(g):8.1f}")
+for mode in ("w", "wr", "none"):
+    for name, g in graphs.items():
+        print(f"{name:10s} graph us (median, flush={mode}): {timeit(g, mode=mode):8.1f}")
 print("counts", [c.view(-1).tolist()[:2] for c in layer.count] if fused else "")

@@ -2,6 +2,8 @@
 Stage kernels trace as id 10 + l_c; the BSA kernel as id 2."""
 import ctypes as C
 import sys
+from pathlib import Path
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 
 import numpy as np
 import torch
@@ -20,6 +22,9 @@ L = _capi.lib()
 L.hp_trace_enable.argtypes = [C.c_void_p, C.c_int]
 buf = torch.zeros((16384, 8), dtype=torch.int64, device="cuda")
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+flush_rd = torch.ones(512 << 20, dtype=torch.uint8, device="cuda")
+flush_out = torch.empty(1, dtype=torch.int64, device="cuda")
+mode = sys.argv[2] if len(sys.argv) > 2 else "w"
 for _ in range(3):
     layer.run(t)
 torch.cuda.synchronize()
@@ -27,7 +32,10 @@ names = {10 + 256: "stage1", 10 + 32: "stage2", 10 + 8: "stage3", 3: "topk(last 
 for kid, name in names.items():
     buf.zero_()
     _capi.check(L.hp_trace_enable(buf.data_ptr(), kid))
-    flush.zero_()
+    if mode in ("w", "wr"):
+        flush.zero_()
+    if mode == "wr":
+        flush_out.copy_(flush_rd.view(torch.int64).sum().view(1))
     torch.cuda.synchronize()
     layer.run(t)
     torch.cuda.synchronize()
