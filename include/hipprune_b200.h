@@ -266,6 +266,9 @@ int hp_decode_materialize(const hp_list_ref* refs, const int32_t* const* counts,
  * kernels (kernel_id 10 + l_c = stage descent, 3 = top-k, 2 = BSA) into
  * buf [16384][8] u64 (first 8192 rows: timer, next 8192: clock). NULL disables. */
 int hp_trace_enable(unsigned long long* buf, int kernel_id);
+/* Developer instrumentation (dev build only, no-op otherwise): kernel `kernel_id` returns
+ * early at its cut point `at` (-1 disables), to time a kernel prefix in isolation. */
+int hp_debug_cut(int kernel_id, int at);
 
 /* Log-sum-exp merge of per-shard (m, l, o) partials (C5 sequence sharding):
  * m, l [n_shards][n]; o [n_shards][n][d] -> out [n][d]. */

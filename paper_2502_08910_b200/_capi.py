@@ -104,7 +104,7 @@ EXPORTS = ["hp_last_error", "hp_version", "hp_device_available", "hp_build_rope_
            "hp_stage_workspace_bytes", "hp_prune_stage", "hp_remap_blocks",
            "hp_selected_indices", "hp_bsa_workspace_bytes", "hp_bsa", "hp_lse_merge",
            "hp_decode_stage_workspace_bytes", "hp_decode_stage", "hp_decode_bsa_workspace_bytes",
-           "hp_decode_bsa", "hp_decode_materialize", "hp_decode_append", "hp_trace_enable"]
+           "hp_decode_bsa", "hp_decode_materialize", "hp_decode_append", "hp_trace_enable", "hp_debug_cut"]
 
 
 def lib():

@@ -118,6 +118,11 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
 }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
@@ -163,6 +168,31 @@ __device__ __forceinline__ bool kv_row_resident(const hp_kv_view& v, int64_t tok
     return v.page_table[page] >= 0;
 }
 
+// ---- programmatic dependent launch --------------------------------------------------
+// Every decode kernel is launched with programmatic stream serialization: it lets its
+// dependent grid launch as soon as all of its CTAs are running (launch_dependents at
+// the top), and waits for its own predecessor's completion and memory (wait) before
+// touching anything that predecessor wrote. The next kernel's launch and CTA
+// rasterisation then overlap this kernel's tail instead of following it.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // ---- last-CTA ticket ---------------------------------------------------------------
 // Called by all threads after the CTA's global writes. One thread takes the ticket
 // with a gpu-scope acq_rel atomic: release publishes every write the CTA made
@@ -188,11 +218,26 @@ __device__ __forceinline__ bool cta_ticket_last(int* counter, int total, int* sh
 // internal linkage: each translation unit that traces exports its own enable call
 static __device__ unsigned long long* g_trace_buf = nullptr;
 static __device__ int g_trace_kernel = -1;
+static __device__ int g_cut_kernel = -1;  // dev build: early exit of kernel id at cut point
+static __device__ int g_cut_at = -1;
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
 }
+// Phase-cut experiments (dev build only): returns true when kernel `kernel_id` should
+// stop at cut point `at`, to time a kernel's prefix in isolation.
+// Load once per kernel (dev_cut_point) and compare in registers: a global load per
+// check would itself add a memory round trip at every cut point.
+__device__ __forceinline__ int dev_cut_point(int kernel_id) {
+#ifdef HP_TRACE
+    return g_cut_kernel == kernel_id ? g_cut_at : -1;
+#else
+    (void)kernel_id;
+    return -1;
+#endif
+}
+
 // Compiled in only with -DHP_TRACE (the dev build `HP_TRACE=1 python -m
 // paper_2502_08910_b200.build`): the enable check is a global load per call site.
 __device__ __forceinline__ void trace(int kernel_id, int slot) {

@@ -331,6 +331,8 @@ __device__ void cta_topk_smem(const uint32_t* keys, int cc, int K, int32_t* sel,
 template <typename T, bool EXT>
 __global__ void __launch_bounds__(kStageWarps * 32, 6)
 decode_stage_kernel(const hp_decode_stage_args a, float* scores, int* tickets, int cg, int prefetch) {
+    pdl_trigger();
+    pdl_wait();
     extern __shared__ __align__(128) unsigned char smem[];
     using G = RowGeom<T>;
     const int hpm = a.heads_per_mask;
@@ -488,6 +490,8 @@ constexpr int kTopkMaxKeys = 16384;
 
 __global__ void __launch_bounds__(kTopkThreads2)
 decode_topk_kernel(const hp_decode_stage_args a, const float* scores) {
+    pdl_trigger();
+    pdl_wait();
     extern __shared__ __align__(16) unsigned char tsm[];
     __shared__ TopkShared sh;
     const int m = blockIdx.x, t = threadIdx.x, nt = blockDim.x;
@@ -575,26 +579,31 @@ struct BsaSmem {
     static constexpr size_t p_off = q_off + HC * kD * 4;
     static constexpr size_t r_off = p_off + HC * kBsaMaxKeys * 4;
     static constexpr size_t ml_off = r_off + 4 * HC * kD * 4;
-    static constexpr size_t tok_off = ml_off + ((2 * HC * 4 + 15) / 16) * 16;
-    static constexpr size_t bytes = tok_off + kBsaMaxKeys * 4;
+    static constexpr size_t ptr_off = ml_off + ((2 * HC * 4 + 15) / 16) * 16;
+    static constexpr size_t bytes = ptr_off + 2 * kBsaMaxKeys * 8;
     // merge scratch reuses the K rows: (m, l) pairs of every split
     static constexpr int max_merge_pairs = static_cast<int>((v_off - k_off) / 8);
 };
 
 template <typename T, int HC, bool EXT>
-__global__ void __launch_bounds__(kBsaThreads, 2)
+__global__ void __launch_bounds__(kBsaThreads, 1)
 decode_bsa_kernel(const hp_decode_bsa_args a, float* part, int* tickets, int splits, int kpc) {
+    pdl_trigger();
+    pdl_wait();
     using S = BsaSmem<T, HC>;
     constexpr int RB = S::RB, KS = S::KS;
     constexpr int half = kD / 2;
     extern __shared__ __align__(128) unsigned char smem[];
+    const int cut = dev_cut_point(2);
+    if (cut == 0) return;
     unsigned char* Ks = smem + S::k_off;
     unsigned char* Vs = smem + S::v_off;
     float* qs = reinterpret_cast<float*>(smem + S::q_off);
     float* ps = reinterpret_cast<float*>(smem + S::p_off);
     float* red = reinterpret_cast<float*>(smem + S::r_off);
     float* ml = reinterpret_cast<float*>(smem + S::ml_off);
-    int32_t* toks = reinterpret_cast<int32_t*>(smem + S::tok_off);
+    unsigned long long* kptr = reinterpret_cast<unsigned long long*>(smem + S::ptr_off);  // row addresses
+    unsigned long long* vptr = kptr + kBsaMaxKeys;
     __shared__ int sh_last;
 
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
@@ -620,27 +629,31 @@ decode_bsa_kernel(const hp_decode_bsa_args a, float* part, int* tickets, int spl
         const int64_t tok = p < sink_end ? p
                             : p < sink_end + n_mask ? ref_token(a.mask, mask, p - sink_end)
                                                     : stream_begin + (p - sink_end - n_mask);
-        toks[t] = static_cast<int32_t>(tok);
+        kptr[t] = reinterpret_cast<unsigned long long>(kv_row_ptr(a.kv, a.kv.k_pool, a.kv.k_host, kvh, tok, sizeof(T)));
+        vptr[t] = reinterpret_cast<unsigned long long>(kv_row_ptr(a.kv, a.kv.v_pool, a.kv.v_host, kvh, tok, sizeof(T)));
     }
+    if (cut == 5) return;
     for (int i = t; i < HC * kD; i += kBsaThreads) qs[i] = a.q[static_cast<int64_t>(h0) * kD + i];
     __syncthreads();
+    if (cut == 6) return;
     {
-        constexpr int CH = RB / 16;  // 16-byte chunks per row: 16 (bf16) or 32 (fp32)
-        for (int r = w; r < nv; r += kBsaThreads / 32) {
-            const int64_t tok = toks[r];
-            if constexpr (CH == 16) {
-                const bool isv = lane >= 16;
-                const int c = lane & 15;
-                const char* src = kv_row_ptr(a.kv, isv ? a.kv.v_pool : a.kv.k_pool, isv ? a.kv.v_host : a.kv.k_host,
-                                             kvh, tok, sizeof(T));
-                cp_async16((isv ? Vs + r * RB : Ks + r * KS) + c * 16, src + c * 16);
-            } else {
-                const char* ks = kv_row_ptr(a.kv, a.kv.k_pool, a.kv.k_host, kvh, tok, sizeof(T));
-                const char* vs = kv_row_ptr(a.kv, a.kv.v_pool, a.kv.v_host, kvh, tok, sizeof(T));
-                cp_async16(Ks + r * KS + lane * 16, ks + lane * 16);
-                cp_async16(Vs + r * RB + lane * 16, vs + lane * 16);
-            }
+        // K rows first (group 0), then V rows (group 1): QK starts while V is in flight.
+        // bf16: a warp instruction moves two 256 B rows (16 lanes each); fp32: one.
+        constexpr int CH = RB / 16;
+        constexpr int RPI = 32 / CH;
+        const int c = lane % CH, sub = lane / CH;
+#pragma unroll
+        for (int i = 0; i < kBsaMaxKeys / (kBsaThreads / 32) / RPI; ++i) {
+            const int r = (i * (kBsaThreads / 32) + w) * RPI + sub;
+            if (r < nv) cp_async16(Ks + r * KS + c * 16, reinterpret_cast<const char*>(kptr[r]) + c * 16);
         }
+        cp_async_commit();
+#pragma unroll
+        for (int i = 0; i < kBsaMaxKeys / (kBsaThreads / 32) / RPI; ++i) {
+            const int r = (i * (kBsaThreads / 32) + w) * RPI + sub;
+            if (r < nv) cp_async16(Vs + r * RB + c * 16, reinterpret_cast<const char*>(vptr[r]) + c * 16);
+        }
+        cp_async_commit();
     }
     if constexpr (EXT) {  // q at its true position (sparse_attention.cpp:47)
         __syncthreads();
@@ -655,13 +668,15 @@ decode_bsa_kernel(const hp_decode_bsa_args a, float* part, int* tickets, int spl
         }
     }
     trace(2, 1);
-    cp_async_wait_all();
+    if (cut == 7) return;
+    cp_async_wait_group<1>();  // K rows landed
     __syncthreads();
     trace(2, 2);
+    if (cut == 1) return;
 
-    // ---- 2. QK: key j = w*16 + (lane & 15), elements [hf*64, hf*64 + 64)
-    {
-        const int j = w * 16 + (lane & 15), hf = lane >> 4;
+    // ---- 2. QK: key j = jb + w*16 + (lane & 15), elements [hf*64, hf*64 + 64)
+    for (int jb = 0; jb < kpc; jb += (kBsaThreads / 32) * 16) {
+        const int j = jb + w * 16 + (lane & 15), hf = lane >> 4;
         float acc[HC];
 #pragma unroll
         for (int hh = 0; hh < HC; ++hh) acc[hh] = 0.f;
@@ -718,6 +733,7 @@ decode_bsa_kernel(const hp_decode_bsa_args a, float* part, int* tickets, int spl
     }
     __syncthreads();
     trace(2, 3);
+    if (cut == 2) return;
     // ---- 3. softmax pieces per head
     if (w < HC) {
         float* pr = ps + w * kBsaMaxKeys;
@@ -734,6 +750,7 @@ decode_bsa_kernel(const hp_decode_bsa_args a, float* part, int* tickets, int spl
         l = warp_sum(l);
         if (lane == 0) { ml[2 * w] = mx; ml[2 * w + 1] = l; }
     }
+    cp_async_wait_all();  // V rows landed
     __syncthreads();
     // ---- PV: element pair d2, key quarter kq
     {
@@ -766,6 +783,7 @@ decode_bsa_kernel(const hp_decode_bsa_args a, float* part, int* tickets, int spl
     }
     __syncthreads();
     trace(2, 4);
+    if (cut == 3) return;
     float* pbase = part + static_cast<int64_t>(hg) * splits * HC * (kD + 2);
     for (int idx = t; idx < HC * kD; idx += kBsaThreads) {
         const int hh = idx / kD, e = idx - hh * kD;
@@ -775,6 +793,7 @@ decode_bsa_kernel(const hp_decode_bsa_args a, float* part, int* tickets, int spl
         if (e == 0) { pp[0] = ml[2 * hh]; pp[1] = ml[2 * hh + 1]; }
         pp[2 + e] = o;
     }
+    if (cut == 4) return;
     const bool last_cta = cta_ticket_last(&tickets[hg], splits, &sh_last);
     trace(2, 6);
     if (!last_cta) return;
@@ -841,6 +860,8 @@ struct MatArgs {
 };
 
 __global__ void materialize_kernel(const MatArgs a) {
+    pdl_trigger();
+    pdl_wait();
     const int l = blockIdx.z, m = blockIdx.y;
     const int64_t n = a.count[l][m];
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
@@ -873,12 +894,14 @@ cudaError_t launch_stage(const hp_decode_stage_args& a, float* scores, int* tick
     // speculative next-row prefetch only where the stage is latency-bound (few descents)
     const int64_t lanes = static_cast<int64_t>(a.n_masks) * a.max_chunks * hpm;
     const int prefetch = lanes <= 65536 ? 1 : 0;
-    kern<<<grid, threads, smem, s>>>(a, scores, tickets, cg, prefetch);
+    e = launch_pdl(kern, grid, dim3(threads), smem, s, a, scores, tickets, cg, prefetch);
+    if (e != cudaSuccess) return e;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     const size_t tsmem = static_cast<size_t>(kTopkMaxKeys) * 4 + static_cast<size_t>(kTopkMaxKeys) * 4;  // keys + kept ids
     e = cudaFuncSetAttribute(decode_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(tsmem));
     if (e != cudaSuccess) return e;
-    decode_topk_kernel<<<a.n_masks, kTopkThreads2, tsmem, s>>>(a, scores);
+    e = launch_pdl(decode_topk_kernel, dim3(a.n_masks), dim3(kTopkThreads2), tsmem, s, a, scores);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
@@ -889,7 +912,8 @@ cudaError_t launch_bsa(const hp_decode_bsa_args& a, float* part, int* tickets, i
     auto kern = decode_bsa_kernel<T, HC, EXT>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(S::bytes));
     if (e != cudaSuccess) return e;
-    kern<<<dim3(splits, a.n_q_heads / HC), kBsaThreads, S::bytes, s>>>(a, part, tickets, splits, kpc);
+    e = launch_pdl(kern, dim3(splits, a.n_q_heads / HC), dim3(kBsaThreads), S::bytes, s, a, part, tickets, splits, kpc);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
@@ -916,6 +940,11 @@ int bsa_keys_per_cta(int64_t max_sel, int groups) {
 
 // Developer instrumentation: record per-CTA phase stamps of kernel `kernel_id`
 // (1 = decode stage, 2 = decode BSA) into buf [n_cta][8] (NULL disables).
+extern "C" int hp_debug_cut(int kernel_id, int at) {
+    if (int rc = hph::check_cuda(cudaMemcpyToSymbol(g_cut_kernel, &kernel_id, sizeof(int)), "hp_debug_cut")) return rc;
+    return hph::check_cuda(cudaMemcpyToSymbol(g_cut_at, &at, sizeof(int)), "hp_debug_cut");
+}
+
 extern "C" int hp_trace_enable(unsigned long long* buf, int kernel_id) {
     if (int rc = hph::check_cuda(cudaMemcpyToSymbol(g_trace_buf, &buf, sizeof(buf)), "hp_trace_enable")) return rc;
     return hph::check_cuda(cudaMemcpyToSymbol(g_trace_kernel, &kernel_id, sizeof(int)), "hp_trace_enable");
@@ -1006,6 +1035,8 @@ extern "C" int hp_decode_bsa(const hp_decode_bsa_args* ap, void* stream) {
 
 __global__ void append_kernel(const hp_kv_view kv, const unsigned char* k_rows,
                               const unsigned char* v_rows, int64_t token, int32_t* keys_exact) {
+    pdl_trigger();
+    pdl_wait();
     const int eb = kv.dtype == HP_BF16 ? 2 : 4;
     const int row_bytes = kv.d * eb;
     const int h = blockIdx.x;
@@ -1033,8 +1064,10 @@ extern "C" int hp_decode_append(const hp_kv_view* kv, const void* k_rows, const 
     if (!kv || !k_rows) return hph::set_error(HP_INVALID_ARGUMENT, "hp_decode_append: null pointer");
     if (token < 0 || token >= static_cast<int64_t>(kv->num_pages) * kv->page_size)
         return hph::set_error(HP_OUT_OF_RANGE, "hp_decode_append: token beyond the cache capacity");
-    append_kernel<<<kv->n_kv, 128, 0, static_cast<cudaStream_t>(stream)>>>(
-        *kv, static_cast<const unsigned char*>(k_rows), static_cast<const unsigned char*>(v_rows), token, keys_exact);
+    const cudaError_t e = launch_pdl(append_kernel, dim3(kv->n_kv), dim3(128), 0, static_cast<cudaStream_t>(stream), *kv,
+                                     static_cast<const unsigned char*>(k_rows), static_cast<const unsigned char*>(v_rows),
+                                     token, keys_exact);
+    if (e != cudaSuccess) return hph::check_cuda(e, "append_kernel");
     return hph::check_cuda(cudaGetLastError(), "append_kernel");
 }
 
@@ -1051,6 +1084,8 @@ extern "C" int hp_decode_materialize(const hp_list_ref* refs, const int32_t* con
         m.stride[i] = out_strides[i];
     }
     const int blocks = std::max(1, std::min(64, (max_count + 255) / 256));
-    materialize_kernel<<<dim3(blocks, n_masks, n_lists), 256, 0, static_cast<cudaStream_t>(stream)>>>(m);
+    const cudaError_t e = launch_pdl(materialize_kernel, dim3(blocks, n_masks, n_lists), dim3(256), 0,
+                                     static_cast<cudaStream_t>(stream), m);
+    if (e != cudaSuccess) return hph::check_cuda(e, "materialize_kernel");
     return hph::check_cuda(cudaGetLastError(), "materialize_kernel");
 }

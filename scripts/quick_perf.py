@@ -58,6 +58,21 @@ def timeit(g, n=20, mode="w"):
         ts.append(a.elapsed_time(b) * 1e3)
     ts.sort()
     return ts[len(ts) // 2]
+# marginal cost: a graph with the BSA-only step twice, and one with a trivial kernel
+s.wait_stream(torch.cuda.current_stream())
+with torch.cuda.stream(s):
+    layer.run(t, refresh=[False] * 3)
+torch.cuda.current_stream().wait_stream(s)
+g2 = torch.cuda.CUDAGraph()
+with torch.cuda.graph(g2):
+    layer.run(t, refresh=[False] * 3)
+    layer.run(t, refresh=[False] * 3)
+graphs["bsa_x2"] = g2
+tiny = torch.zeros(1, device="cuda")
+g0 = torch.cuda.CUDAGraph()
+with torch.cuda.graph(g0):
+    tiny.add_(1)
+graphs["trivial"] = g0
 for mode in ("w", "wr", "none"):
     for name, g in graphs.items():
         print(f"{name:10s} graph us (median, flush={mode}): {timeit(g, mode=mode):8.1f}")
