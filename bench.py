@@ -50,6 +50,8 @@ def parse():
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--ctx", type=int, default=T_DEFAULT)
+    p.add_argument("--layers", type=int, default=8,
+                   help="layers per decode step (distinct KV each); value = step time / layers")
     p.add_argument("--no-cpu-baseline", action="store_true")
     return p.parse_args()
 
@@ -62,11 +64,13 @@ def dist_env():
 
 
 def config(args, world):
-    return {"workload": f"C3 decode, T={args.ctx}, KV in HBM, full-refresh layer step",
+    return {"workload": f"C3 decode, T={args.ctx}, KV in HBM, full-refresh step over {args.layers} layers "
+                        f"(distinct KV per layer), reported per layer",
             "context": args.ctx, "q_heads": GROUPS * HPM, "kv_heads": GROUPS, "head_dim": D,
             "preset": "3k", "stages": STAGES, "sink": SINK, "stream": STREAM,
             "units_per_gpu": f"{GROUPS} (layer, KV-group) units", "parallelism": f"kv-group x{world}",
-            "l2": "flushed (512 MB write) before every timed step"}
+            "layers_per_step": args.layers,
+            "l2": "flushed before every timed step: 512 MB write, then 512 MB read (dirty lines evicted)"}
 
 
 # --------------------------------------------------------------------- clocks
@@ -187,39 +191,54 @@ def main():
     D_.require_cuda()
 
     t = args.ctx
-    q, k, v = synth.generate(GROUPS * HPM, GROUPS, t, D, t_q=max(16, args.steps + args.warmup),
-                             seed=1 + rank, device=dev)
-    kv = D_.PagedKV(k, v, page_size=64, dtype=torch.bfloat16, device=dev)
-    del k, v
-    layer = D_.FusedDecodeLayer(kv, STAGES, sink=SINK, stream_tokens=STREAM,
-                                n_q_heads=GROUPS * HPM, n_masks=GROUPS, device=dev)
-    qs = q.transpose(0, 1).contiguous()  # [steps, heads, d]: a fresh query per step
+    L = max(1, args.layers)
+    n_q = max(16, args.steps + args.warmup)
+    kvs, layers, qss = [], [], []
+    for li in range(L):
+        q, k, v = synth.generate(GROUPS * HPM, GROUPS, t, D, t_q=n_q, seed=1 + rank * 1000 + li, device=dev)
+        kv = D_.PagedKV(k, v, page_size=64, dtype=torch.bfloat16, device=dev)
+        del k, v
+        kvs.append(kv)
+        layers.append(D_.FusedDecodeLayer(kv, STAGES, sink=SINK, stream_tokens=STREAM,
+                                          n_q_heads=GROUPS * HPM, n_masks=GROUPS, device=dev))
+        qss.append(q.transpose(0, 1).contiguous())  # [steps, heads, d]: a fresh query per step
+    kv, layer, qs = kvs[0], layers[0], qss[0]
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    flush_rd = torch.ones(512 << 20, dtype=torch.uint8, device=dev)
+    flush_sink = torch.empty(1, dtype=torch.int64, device=dev)
 
-    # ---- graphs: one per refresh pattern of the (16, 8, 4) schedule
+    def do_flush():
+        flush.zero_()
+        flush_sink.copy_(flush_rd.view(torch.int64).sum().view(1))
+
+    # ---- graphs: one per refresh pattern of the (16, 8, 4) schedule, all L layers each
     patterns = {"full": (True, True, True), "s23": (False, True, True), "s3": (False, False, True),
                 "bsa": (False, False, False)}
     stream = torch.cuda.Stream(device=dev)
-    layer.q.copy_(qs[0])
-    for _ in range(3):
-        layer.run(t)
+    for ly, qq in zip(layers, qss):
+        ly.q.copy_(qq[0])
+        for _ in range(3):
+            ly.run(t)
     torch.cuda.synchronize()
     graphs = {}
     for name, fl in patterns.items():
         stream.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(stream):
-            layer.run(t, refresh=list(fl))
+            for ly in layers:
+                ly.run(t, refresh=list(fl))
         torch.cuda.current_stream().wait_stream(stream)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=stream):
-            layer.run(t, refresh=list(fl))
+            for ly in layers:
+                ly.run(t, refresh=list(fl))
         graphs[name] = g
     torch.cuda.synchronize()
     cur = torch.cuda.current_stream()
 
     def timed(name, i):
-        layer.q.copy_(qs[i % qs.shape[0]])
-        flush.zero_()
+        for ly, qq in zip(layers, qss):
+            ly.q.copy_(qq[i % qq.shape[0]])
+        do_flush()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(cur)
         graphs[name].replay()
@@ -231,9 +250,8 @@ def main():
         if world > 1:
             torch.distributed.barrier()
 
-    # ---- warmup, then the timed region (full-refresh layer step). The clock sampler
-    # runs across a soak of the same graph so it sees the timed region's clocks even
-    # when K steps last only milliseconds.
+    # ---- warmup, then the timed region (full-refresh step). The clock sampler runs
+    # across a soak of the same graph so it sees the timed region's clocks.
     clocks = ClockSampler(local)
     clocks.start()
     soak_end = time.time() + 1.0
@@ -241,14 +259,14 @@ def main():
     while time.time() < soak_end:
         timed("full", i)
         i += 1
-        if i % 64 == 0:
+        if i % 16 == 0:
             torch.cuda.synchronize()
     for i in range(args.warmup):
         timed("full", i)
     barrier()
     ev = [timed("full", args.warmup + i) for i in range(args.steps)]
     barrier()
-    step_us = [1000.0 * a.elapsed_time(b) for a, b in ev]
+    step_us = [1000.0 * a.elapsed_time(b) / L for a, b in ev]
     # amortized schedule over whole 16-step cycles and the BSA-only step
     sched = []
     ctr = [0, 0, 0]
@@ -260,26 +278,35 @@ def main():
     bsa_ev = [timed("bsa", i) for i in range(args.steps)]
     barrier()
     clk = clocks.stop()
-    amort_us = statistics.mean(1000.0 * a.elapsed_time(b) for a, b in sched)
-    bsa_us = statistics.mean(1000.0 * a.elapsed_time(b) for a, b in bsa_ev)
+    amort_us = statistics.mean(1000.0 * a.elapsed_time(b) / L for a, b in sched)
+    bsa_us = statistics.mean(1000.0 * a.elapsed_time(b) / L for a, b in bsa_ev)
     mean_step = statistics.mean(step_us)
     if world > 1:
         tt = torch.tensor([mean_step, amort_us, bsa_us], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         mean_step, amort_us, bsa_us = tt.tolist()
 
-    # ---- dominant kernel: stage-1 descent + selection, timed alone on its stream
-    layer.q.copy_(qs[0])
+    # ---- dominant kernel: the stage-1 descent (decode_stage_kernel), timed alone on its
+    # stream: a graph of its L per-layer launches, L2 flushed before each replay
+    s1_graph = torch.cuda.CUDAGraph()
+    stream.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(stream):
+        for ly in layers:
+            ly.run_stage(t, 0, select=False)
+    torch.cuda.current_stream().wait_stream(stream)
+    with torch.cuda.graph(s1_graph, stream=stream):
+        for ly in layers:
+            ly.run_stage(t, 0, select=False)
     s1 = []
     for i in range(max(3, args.steps // 2)):
-        flush.zero_()
+        do_flush()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(cur)
-        layer.run_stage(t, 0)
+        s1_graph.replay()
         b.record(cur)
         s1.append((a, b))
     torch.cuda.synchronize()
-    s1_us = statistics.mean(1000.0 * a.elapsed_time(b) for a, b in s1)
+    s1_us = statistics.mean(1000.0 * a.elapsed_time(b) / L for a, b in s1)
     kv.count_rows(True)
     layer.run_stage(t, 0)
     torch.cuda.synchronize()
@@ -300,25 +327,25 @@ def main():
     except Exception:
         pass
 
-    # ---- e2e through the host-facing call: pinned H2D (q + new token K/V) -> step -> D2H
-    e2e_us = None
+    # ---- e2e through the host-facing per-layer call, for every layer of the step:
+    # pinned H2D (q + the new token's K/V) -> append -> layer step -> D2H of the output
     h2d = GROUPS * HPM * D * 4 + 2 * GROUPS * D * 2
     d2h = GROUPS * HPM * D * 4
-    q_host = qs[: min(qs.shape[0], 8)].cpu().pin_memory()
+    q_host = [qq[: min(qq.shape[0], 8)].cpu().pin_memory() for qq in qss]
     krow = torch.randn((GROUPS, D), device=dev).to(torch.bfloat16).cpu().pin_memory()
     vrow = torch.randn((GROUPS, D), device=dev).to(torch.bfloat16).cpu().pin_memory()
-    out_host = torch.empty((GROUPS * HPM, D), dtype=torch.float32).pin_memory()
     e2e = []
     barrier()
     for i in range(args.warmup + args.steps):
-        flush.zero_()
+        do_flush()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(cur)
-        layer.step_host(t, q_host[i % q_host.shape[0]], krow, vrow, sync=False)
+        for ly, qh in zip(layers, q_host):
+            ly.step_host(t, qh[i % qh.shape[0]], krow, vrow, sync=False)
         b.record(cur)
         b.synchronize()
         if i >= args.warmup:
-            e2e.append(1000.0 * a.elapsed_time(b))
+            e2e.append(1000.0 * a.elapsed_time(b) / L)
     e2e_us = statistics.mean(e2e)
     if world > 1:
         tt = torch.tensor([e2e_us], dtype=torch.float64, device=dev)
@@ -345,7 +372,7 @@ def main():
             cpu = {"value": None, "unit": "us/layer", "cores": None, "kind": None, "sample": f"failed: {e}"}
 
     if rank == 0:
-        launches_per_step = 2 * len(STAGES) + 1 + 1  # (descent + select) x 3, BSA, cache materialize
+        launches_per_step = (2 * len(STAGES) + 1 + 1) * L  # per layer: (descent + select) x 3, BSA, materialize
         line = {
             "metric": METRIC, "value": mean_step / world, "unit": "us/layer", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean_step / 1000.0,
@@ -357,7 +384,7 @@ def main():
             "bsa_only_us": bsa_us / world,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "decode_stage_kernel + decode_topk_kernel (stage 1)",
+                         "kernel": "decode_stage_kernel<bf16> (stage-1 descent, 8 KV groups)",
                          "kernel_us": s1_us, "algorithmic_bytes": alg_bytes,
                          "distinct_key_rows": rows, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"},
             "cpu_baseline": cpu,

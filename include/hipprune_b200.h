@@ -208,7 +208,8 @@ typedef struct hp_decode_stage_args {
     int64_t in_count_const;
     int32_t max_chunks;          /* >= ceil(in_count / chunk_size)                      */
     int32_t sel_stride;          /* >= keep / chunk_size                                */
-    int32_t* sel_out;            /* [n_masks][sel_stride] kept chunk ids, ascending     */
+    int32_t* sel_out;            /* [n_masks][sel_stride] kept chunk ids, ascending; NULL =
+                                    descent only (chunk scores left in the workspace)      */
     int32_t* out_count;          /* [n_masks] output list length                        */
     void* workspace;             /* >= hp_decode_stage_workspace_bytes()                */
     size_t workspace_bytes;

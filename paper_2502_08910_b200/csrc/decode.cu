@@ -897,6 +897,7 @@ cudaError_t launch_stage(const hp_decode_stage_args& a, float* scores, int* tick
     e = launch_pdl(kern, grid, dim3(threads), smem, s, a, scores, tickets, cg, prefetch);
     if (e != cudaSuccess) return e;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if (a.sel_out == nullptr) return cudaSuccess;  // descent only: scores stay in the workspace
     const size_t tsmem = static_cast<size_t>(kTopkMaxKeys) * 4 + static_cast<size_t>(kTopkMaxKeys) * 4;  // keys + kept ids
     e = cudaFuncSetAttribute(decode_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(tsmem));
     if (e != cudaSuccess) return e;
@@ -965,7 +966,7 @@ extern "C" int hp_decode_stage(const hp_decode_stage_args* ap, void* stream) {
         a.keys.n_kv <= 0 || a.n_q_heads % a.keys.n_kv)
         return hph::set_error(HP_INVALID_ARGUMENT, "hp_decode_stage: bad head geometry");
     if (a.in.depth < 0 || a.in.depth > 4) return hph::set_error(HP_INVALID_ARGUMENT, "hp_decode_stage: list depth");
-    if (a.sel_stride < a.keep / a.chunk_size) return hph::set_error(HP_INVALID_ARGUMENT, "hp_decode_stage: sel_stride < k/l_c");
+    if (a.sel_out && a.sel_stride < a.keep / a.chunk_size) return hph::set_error(HP_INVALID_ARGUMENT, "hp_decode_stage: sel_stride < k/l_c");
     if (a.max_chunks <= 0) return hph::set_error(HP_INVALID_ARGUMENT, "hp_decode_stage: max_chunks must be >= 1");
     if (a.max_chunks > kTopkMaxKeys)
         return hph::set_error(HP_INVALID_ARGUMENT, "hp_decode_stage: %d chunks per list exceed the fused selection limit %d",

@@ -531,10 +531,10 @@ class FusedDecodeLayer:
                                                   max(self.stages[i][2] for i in idx), sp))
         return self.out
 
-    def run_stage(self, t: int, i: int = 0, stream=None) -> None:
-        """Launch only stage i (descent + selection) on its input: stage 0 reads the
-        range [n_sink, T - n_stream), later stages the materialized cache of i-1.
-        Used to time / instrument the dominant kernel in isolation."""
+    def run_stage(self, t: int, i: int = 0, stream=None, select: bool = True) -> None:
+        """Launch only stage i (descent, + selection unless select=False) on its input:
+        stage 0 reads the range [n_sink, T - n_stream), later stages the materialized
+        cache of i-1. Used to time / instrument the dominant kernel in isolation."""
         (_, lc, keep) = self.stages[i]
         pos = t - 1
         upper = t - self.stream_tokens if t > self.stream_tokens else 0
@@ -547,7 +547,7 @@ class FusedDecodeLayer:
             n_q_heads=self.n_q_heads, stream_tokens=self.stream_tokens, q=_ptr(self.q),
             query_position=pos, in_=in_ref, in_count=_ptr(in_count), in_count_const=const,
             max_chunks=self.max_chunks[i], sel_stride=self.sel[i].shape[-1],
-            sel_out=_ptr(self.sel[i]), out_count=_ptr(self.count[i]),
+            sel_out=_ptr(self.sel[i]) if select else None, out_count=_ptr(self.count[i]),
             workspace=_ptr(self.ws_stage), workspace_bytes=self.ws_stage.numel(),
             keys=self.kv.view(t), rope=self.policy.ctx(self.layer1, self.rope),
             keys_exact=_ptr(self.kv.keys_exact), list_out=None, list_out_stride=0)
