@@ -139,6 +139,14 @@ class Oracle:
                            _szp, _f32p, _sz, _f32p, _f32p, _f32p)
             self.f_counts = f("decode_read_counts", C.c_int, _f32p, _f32p, _sz, _sz, _sz, _szp,
                               _sz, _sz, _sz, C.c_int, _sz, _sz, _u64p, _u64p)
+            self.f_enew = f("engine_new", _vp, _f32p, _f32p, _f32p, _sz, _sz, _sz, _sz, _sz, _sz,
+                            _szp, _sz, _sz, _sz, _szp, C.c_int, _sz, _sz, _sz, _sz, C.c_double,
+                            C.c_double, _sz)
+            self.f_efree = f("engine_free", None, _vp)
+            self.f_eprefill = f("engine_prefill", _vp, _vp, _f32p)
+            self.f_estep = f("engine_step", C.c_int, _vp, _sz, _f32p, C.POINTER(C.c_int),
+                             C.POINTER(C.c_double), C.POINTER(C.c_double), _u64p, _szp)
+            self.f_ecache = f("engine_stage_cache", _vp, _vp, _sz, _sz)
 
     # ---------------------------------------------------------------- helpers
     def _raise(self):
@@ -321,9 +329,61 @@ class Oracle:
                                   int(ext), layer1, cutoff, _p(dis, _u64p), _p(tot, _u64p)))
         return dis.astype(np.int64), tot.astype(np.int64)
 
+    def engine(self, q, k, v, *, prefill_len, q_len, stages, sink, stream, refresh, ext=False,
+               cutoff=3, page_size=16, mask_cap=64, sa_cap=64):
+        """The reference DecodeEngine (decode.cpp:104-289) over a full workload
+        q, k, v [layers, heads, T, d] (one query per position)."""
+        assert self.kind == "reference"
+        return _Engine(self, q, k, v, prefill_len, q_len, stages, sink, stream, refresh, ext,
+                       cutoff, page_size, mask_cap, sa_cap)
+
     # ------------------------------------------------------------------ store
     def store(self, num_layers, page_size, mask_cap, sa_cap):
         return _Store(self, num_layers, page_size, mask_cap, sa_cap)
+
+
+class _Engine:
+    def __init__(self, o: Oracle, q, k, v, prefill_len, q_len, stages, sink, stream, refresh, ext,
+                 cutoff, page_size, mask_cap, sa_cap):
+        self.o = o
+        self.q, self.k, self.v = _f32(q), _f32(k), _f32(v)
+        L, H, T, d = self.q.shape
+        self.shape = (L, H, d)
+        self.n_stages = len(stages)
+        st = _szarr([x for s_ in stages for x in s_])
+        rf = _szarr(list(refresh))
+        self.h = o.f_enew(_p(self.q, _f32p), _p(self.k, _f32p), _p(self.v, _f32p), L, H, T, d,
+                          prefill_len, q_len, st, len(stages), sink, stream, rf, int(ext), cutoff,
+                          page_size, mask_cap, sa_cap, 1.0, 31.5, 0)
+        if not self.h:
+            o._raise()
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.o.f_efree(self.h)
+            self.h = None
+
+    def prefill(self):
+        h = self.o.f_eprefill(self.h, None)
+        if not h:
+            self.o._raise()
+        return self.o._take_lists(h)
+
+    def step(self, token_index):
+        L, H, d = self.shape
+        n = self.n_stages
+        out = np.zeros((L, H, d), np.float32)
+        refreshed = (C.c_int * n)()
+        lat = (C.c_double * n)()
+        bsa = C.c_double()
+        c4 = np.zeros(4, np.uint64)
+        sizes = (C.c_size_t * n)()
+        self.o._check(self.o.f_estep(self.h, token_index, _p(out, _f32p), refreshed, lat,
+                                     C.byref(bsa), _p(c4, _u64p), sizes))
+        return out, [bool(x) for x in refreshed], list(sizes)
+
+    def stage_cache(self, layer, stage):
+        return self.o._take_lists(self.o.f_ecache(self.h, layer, stage))[0]
 
 
 class _Store:

@@ -59,8 +59,42 @@ def build_cuda(force: bool = False, verbose: bool = False) -> Path:
     return out
 
 
+HOST_SOURCES = ["host/host.cpp", "host/decode_engine.cpp"]
+
+
+def _cuda_home() -> Path:
+    return Path(nvcc()).resolve().parent.parent
+
+
+def build_host(force: bool = False) -> Path:
+    """The C++ host layer (include/hipprune_b200.hpp) over the C ABI, and the
+    reference-named pybind11 module _hipprune on top of it."""
+    import sysconfig
+    import pybind11
+    cuda = _cuda_home()
+    cxx = os.environ.get("CXX", "g++")
+    host = LIB / "libhipprune_host.so"
+    deps = [CSRC / s for s in HOST_SOURCES] + [ROOT / "include" / "hipprune_b200.hpp",
+                                             ROOT / "include" / "hipprune_b200.h", LIB / "libhipprune_b200.so"]
+    common = ["-O2", "-std=c++20", "-fPIC", "-ffp-contract=off", f"-I{ROOT / 'include'}", f"-I{cuda / 'include'}"]
+    links = [f"-L{LIB}", "-lhipprune_b200", f"-L{cuda / 'lib64'}", "-lcudart", "-lz", "-Wl,-rpath,$ORIGIN",
+             f"-Wl,-rpath,{cuda / 'lib64'}"]
+    if force or _stale(host, deps):
+        subprocess.run([cxx, *common, "-shared", *[str(CSRC / s) for s in HOST_SOURCES], "-o", str(host), *links],
+                       check=True)
+    ext = LIB / ("_hipprune" + sysconfig.get_config_var("EXT_SUFFIX"))
+    bdeps = [CSRC / "host" / "bindings.cpp", host]
+    if force or _stale(ext, bdeps):
+        subprocess.run([cxx, *common, "-shared", f"-I{pybind11.get_include()}",
+                        f"-I{sysconfig.get_paths()['include']}", str(CSRC / "host" / "bindings.cpp"), "-o", str(ext),
+                        f"-L{LIB}", "-lhipprune_host", *links], check=True)
+    return ext
+
+
 def build(force: bool = False) -> None:
     build_cuda(force=force)
+    if os.environ.get("HP_TRACE") != "1":
+        build_host(force=force)
 
 
 if __name__ == "__main__":

@@ -96,6 +96,34 @@ def main() -> None:
         out[f"lru{i}_stats"] = np.asarray(st.stats(0), np.int64)
     np.savez_compressed(HERE / "reference_golden.npz", **out)
     print("wrote", HERE / "reference_golden.npz", len(out), "arrays")
+    engine_golden(R)
+
+
+def engine_golden(R) -> None:
+    """5. The reference DecodeEngine (decode.cpp:104-289): prefill, then 12 steps with
+    a (4, 2) refresh schedule; per step the outputs, refresh flags and every
+    (layer, stage) cache — the stage-cache scheduler of DecodeEngine::step."""
+    out = {}
+    q, k, v = R.generate(heads=2, layers=2, seq_kv=640, seq_q=640, dim=16, seed=21)
+    out["q"], out["k"], out["v"] = q, k, v
+    stages = [(16, 8, 128), (16, 4, 64)]
+    out["stages"] = np.asarray(stages, np.int64)
+    out["meta"] = np.asarray([600, 32, 16, 32, 4, 2, 12], np.int64)  # prefill, q_len, sink, stream, refresh, steps
+    for ext in (0, 1):
+        e = R.engine(q, k, v, prefill_len=600, q_len=32, stages=stages, sink=16, stream=32, refresh=[4, 2],
+                     ext=bool(ext))
+        masks = e.prefill()
+        for b, m in enumerate(masks):
+            out[f"e{ext}_prefill_mask{b}"] = m
+        for i in range(12):
+            o, refreshed, _ = e.step(600 + i)
+            out[f"e{ext}_s{i}_out"] = o
+            out[f"e{ext}_s{i}_refreshed"] = np.asarray(refreshed, np.int64)
+            for layer in range(2):
+                for st in range(2):
+                    out[f"e{ext}_s{i}_cache{layer}{st}"] = e.stage_cache(layer, st)
+    np.savez_compressed(HERE / "engine_golden.npz", **out)
+    print("wrote", HERE / "engine_golden.npz", len(out), "arrays")
 
 
 if __name__ == "__main__":
