@@ -271,6 +271,40 @@ int hp_trace_enable(unsigned long long* buf, int kernel_id);
  * early at its cut point `at` (-1 disables), to time a kernel prefix in isolation. */
 int hp_debug_cut(int kernel_id, int at);
 
+/* ------------------------------------------------------------------------ *
+ * On-GPU LRU page cache over a pinned host tier (replaces TieredKvStore::
+ * access_pages / commit and KvView::account, kv_store.cpp:58-120,188-200).
+ * Point an hp_kv_view at it (k_pool = k_slots, k_host = k_host, page_table,
+ * touched): every gather then reads resident pages from their slot and missing
+ * pages from the mapped host tier in the same kernel, flagging touched[page]
+ * (1 hit, 2 miss). hp_cache_commit is the step-end commit: hits take `stamp`,
+ * misses are installed into the least-recently-used slots (host -> slot copies
+ * on the device), stats[0..2] += hits, misses, evictions, touched is cleared.
+ * stamp 0 = use (and advance) a step clock kept in the workspace, so a captured
+ * CUDA graph can replay the commit; explicit stamps must be > 1 (1 = warm start).
+ * The workspace must be zeroed before first use.
+ * ------------------------------------------------------------------------ */
+typedef struct hp_page_cache {
+    void* k_slots;               /* [num_slots][n_kv][page_size][d] device             */
+    void* v_slots;               /* same, or NULL (key-only cache)                      */
+    const void* k_host;          /* [num_pages][n_kv][page_size][d] pinned, device-mapped */
+    const void* v_host;
+    int32_t* page_table;         /* [num_pages] page -> slot, -1 = host only            */
+    int32_t* slot_page;          /* [num_slots] slot -> page, -1 = free                 */
+    uint32_t* slot_stamp;        /* [num_slots] logical time of last use (0 = free)     */
+    uint8_t* touched;            /* [num_pages] per-step access flags                   */
+    int32_t num_pages;
+    int32_t num_slots;           /* <= 16384 */
+    int32_t page_size;
+    int32_t n_kv;
+    int32_t d;
+    int32_t dtype;               /* hp_dtype */
+} hp_page_cache;
+
+size_t hp_cache_workspace_bytes(int32_t num_pages, int32_t num_slots);
+int hp_cache_commit(const hp_page_cache* cache, uint32_t stamp, int32_t* stats, void* workspace,
+                    size_t workspace_bytes, void* stream);
+
 /* Log-sum-exp merge of per-shard (m, l, o) partials (C5 sequence sharding):
  * m, l [n_shards][n]; o [n_shards][n][d] -> out [n][d]. */
 int hp_lse_merge(const float* m, const float* l, const float* o, int32_t n_shards, int32_t n,

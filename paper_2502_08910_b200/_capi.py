@@ -97,6 +97,14 @@ class DecodeBsaArgs(C.Structure):
                 ("workspace_bytes", C.c_size_t), ("kv", KvView), ("rope", RopeCtx)]
 
 
+class PageCache(C.Structure):
+    _fields_ = [("k_slots", C.c_void_p), ("v_slots", C.c_void_p), ("k_host", C.c_void_p),
+                ("v_host", C.c_void_p), ("page_table", C.c_void_p), ("slot_page", C.c_void_p),
+                ("slot_stamp", C.c_void_p), ("touched", C.c_void_p), ("num_pages", C.c_int32),
+                ("num_slots", C.c_int32), ("page_size", C.c_int32), ("n_kv", C.c_int32),
+                ("d", C.c_int32), ("dtype", C.c_int32)]
+
+
 _lib = None
 
 # every symbol include/hipprune_b200.h declares
@@ -104,7 +112,8 @@ EXPORTS = ["hp_last_error", "hp_version", "hp_device_available", "hp_build_rope_
            "hp_stage_workspace_bytes", "hp_prune_stage", "hp_remap_blocks",
            "hp_selected_indices", "hp_bsa_workspace_bytes", "hp_bsa", "hp_lse_merge",
            "hp_decode_stage_workspace_bytes", "hp_decode_stage", "hp_decode_bsa_workspace_bytes",
-           "hp_decode_bsa", "hp_decode_materialize", "hp_decode_append", "hp_trace_enable", "hp_debug_cut"]
+           "hp_decode_bsa", "hp_decode_materialize", "hp_decode_append", "hp_trace_enable", "hp_debug_cut",
+           "hp_cache_workspace_bytes", "hp_cache_commit"]
 
 
 def lib():
@@ -152,6 +161,11 @@ def lib():
     L.hp_decode_append.restype = C.c_int
     L.hp_decode_append.argtypes = [C.POINTER(KvView), C.c_void_p, C.c_void_p, C.c_int64,
                                    C.c_void_p, C.c_void_p]
+    L.hp_cache_workspace_bytes.restype = C.c_size_t
+    L.hp_cache_workspace_bytes.argtypes = [C.c_int32, C.c_int32]
+    L.hp_cache_commit.restype = C.c_int
+    L.hp_cache_commit.argtypes = [C.POINTER(PageCache), C.c_uint32, C.c_void_p, C.c_void_p,
+                                  C.c_size_t, C.c_void_p]
     L.hp_lse_merge.restype = C.c_int
     L.hp_lse_merge.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
                                C.c_int32, C.c_void_p, C.c_void_p]

@@ -607,3 +607,84 @@ class FusedDecodeLayer:
     def mask(self, stage: int = -1):
         """Materialized stage cache (lists, counts) — DecodeEngine::stage_cache."""
         return self.cache[stage], self.count[stage]
+
+
+# ------------------------------------------------------------ page cache (K6)
+class CachedKV(PagedKV):
+    """Paged K/V of one layer held in pinned host memory with an on-GPU LRU page
+    cache of ``num_slots`` pages in front of it (TieredKvStore over the host tier,
+    kv_store.cpp:58-120). Gathers read resident pages from their device slot and
+    missing pages from the mapped host tier inside the same kernel, flagging the
+    page; ``commit()`` (the step-end commit) installs the missed pages into the
+    least-recently-used slots. Drop-in for PagedKV in the decode layers.
+
+    warm: "recent" makes the last ``num_slots`` pages resident at start (the
+    prefill's working set around the stream window), "none" starts empty.
+    """
+
+    def __init__(self, k: torch.Tensor, v: torch.Tensor | None, *, num_slots: int, page_size: int = 64,
+                 dtype: torch.dtype = torch.bfloat16, capacity: int | None = None, device="cuda",
+                 warm: str = "recent"):
+        super().__init__(k, v, page_size=page_size, dtype=dtype, capacity=capacity, device=device)
+        dev = torch.device(device)
+        # host tier (authoritative, pinned, device-mapped under UVA) and the device slots
+        self.k_host = self.k_pool.cpu().pin_memory()
+        self.v_host = self.v_pool.cpu().pin_memory() if self.v_pool is not None else None
+        self.num_slots = int(min(num_slots, self.num_pages))
+        shape = (self.num_slots, self.n_kv, page_size, self.d)
+        self.k_slots = torch.zeros(shape, dtype=dtype, device=dev)
+        self.v_slots = torch.zeros(shape, dtype=dtype, device=dev) if v is not None else None
+        self.page_table = torch.full((self.num_pages,), -1, dtype=torch.int32, device=dev)
+        self.slot_page = torch.full((self.num_slots,), -1, dtype=torch.int32, device=dev)
+        self.slot_stamp = torch.zeros((self.num_slots,), dtype=torch.int32, device=dev)
+        self.touched = torch.zeros((self.num_pages,), dtype=torch.uint8, device=dev)
+        self.stats = torch.zeros(3, dtype=torch.int32, device=dev)  # hits, misses, evictions
+        self.ws_cache = torch.zeros(lib().hp_cache_workspace_bytes(self.num_pages, self.num_slots),
+                                    dtype=torch.uint8, device=dev)
+        self.stamp = 1
+        if warm == "recent":
+            used = ceil_div(self.t_kv, page_size)
+            first = max(0, used - self.num_slots)
+            pages = torch.arange(first, used, device=dev, dtype=torch.int32)
+            n = pages.numel()
+            self.page_table[first:used] = torch.arange(n, device=dev, dtype=torch.int32)
+            self.slot_page[:n] = pages
+            self.slot_stamp[:n] = 1
+            self.k_slots[:n].copy_(self.k_pool[first:used])
+            if self.v_slots is not None:
+                self.v_slots[:n].copy_(self.v_pool[first:used])
+        # the full device pools were only needed to build the tiers
+        self.k_pool_full, self.v_pool_full = self.k_pool, self.v_pool
+        self.k_pool, self.v_pool = self.k_slots, self.v_slots
+        del self.k_pool_full, self.v_pool_full
+
+    def view(self, t_kv: int | None = None) -> KvView:
+        return KvView(k_pool=_ptr(self.k_slots), v_pool=_ptr(self.v_slots), k_host=self.k_host.data_ptr(),
+                      v_host=self.v_host.data_ptr() if self.v_host is not None else None,
+                      page_table=_ptr(self.page_table), touched=_ptr(self.touched),
+                      num_pages=self.num_pages, page_size=self.page_size, n_kv=self.n_kv, d=self.d,
+                      dtype=_DT[self.dtype], t_kv=t_kv if t_kv is not None else self.t_kv,
+                      row_bits=_ptr(self.row_bits), row_bits_stride=self.num_pages * self.page_size)
+
+    def cache_struct(self):
+        return _capi.PageCache(k_slots=_ptr(self.k_slots), v_slots=_ptr(self.v_slots),
+                               k_host=self.k_host.data_ptr(),
+                               v_host=self.v_host.data_ptr() if self.v_host is not None else None,
+                               page_table=_ptr(self.page_table), slot_page=_ptr(self.slot_page),
+                               slot_stamp=_ptr(self.slot_stamp), touched=_ptr(self.touched),
+                               num_pages=self.num_pages, num_slots=self.num_slots,
+                               page_size=self.page_size, n_kv=self.n_kv, d=self.d, dtype=_DT[self.dtype])
+
+    def commit(self, stream=None) -> None:
+        """Step-end commit (decode.cpp:279-280): hits take this step's stamp, misses
+        are installed into the LRU slots. Uses the device step clock (stamp 0), so a
+        captured CUDA graph replays it correctly."""
+        self._cache_s = self.cache_struct()
+        check(lib().hp_cache_commit(C.byref(self._cache_s), 0, _ptr(self.stats), _ptr(self.ws_cache),
+                                    self.ws_cache.numel(), C.c_void_p(_stream(stream))))
+
+    def append(self, k_row, v_row=None):
+        raise NotImplementedError("CachedKV: append through hp_decode_append (write-through to the host tier)")
+
+    def resident_pages(self) -> int:
+        return int((self.page_table >= 0).sum())
