@@ -224,10 +224,24 @@ typedef struct hp_decode_stage_args {
      * i < out_count[m] (resolved through `in`), so a consumer needs no chain hops */
     int32_t* list_out;
     int64_t list_out_stride;
+    /* optional: chunk scores (max over the mask's heads) land here, [n_masks][max_chunks],
+     * instead of the workspace — with sel_out == NULL this is the descent of one shard of
+     * a sequence-sharded stage, selected globally by hp_select_topk */
+    float* scores_out;
 } hp_decode_stage_args;
 
 size_t hp_decode_stage_workspace_bytes(int32_t n_masks, int32_t max_chunks);
 int hp_decode_stage(const hp_decode_stage_args* args, void* stream);
+
+/* The stage's chunk selection on its own (run_pruning_stage's stable top-K,
+ * pruning.cpp:187-192): per mask, keep the keep/chunk_size best of ceil(n_in/chunk_size)
+ * scores (score desc, chunk asc), kept chunk ids ascending in sel_out, the stage output
+ * length in out_count (identity when n_in <= keep). scores [n_masks][stride];
+ * n_in: device counts [n_masks] or NULL => n_in_const. For sequence sharding: the
+ * all-gathered scores of every shard give every rank the same global selection. */
+int hp_select_topk(const float* scores, int64_t stride, int32_t n_masks, const int32_t* n_in,
+                   int64_t n_in_const, int32_t chunk_size, int32_t keep, int32_t* sel_out,
+                   int32_t sel_stride, int32_t* out_count, void* stream);
 
 typedef struct hp_decode_bsa_args {
     int32_t n_q_heads;

@@ -85,7 +85,7 @@ class DecodeStageArgs(C.Structure):
                 ("out_count", C.c_void_p), ("workspace", C.c_void_p),
                 ("workspace_bytes", C.c_size_t), ("keys", KvView), ("rope", RopeCtx),
                 ("keys_exact", C.c_void_p), ("list_out", C.c_void_p),
-                ("list_out_stride", C.c_int64)]
+                ("list_out_stride", C.c_int64), ("scores_out", C.c_void_p)]
 
 
 class DecodeBsaArgs(C.Structure):
@@ -113,7 +113,7 @@ EXPORTS = ["hp_last_error", "hp_version", "hp_device_available", "hp_build_rope_
            "hp_selected_indices", "hp_bsa_workspace_bytes", "hp_bsa", "hp_lse_merge",
            "hp_decode_stage_workspace_bytes", "hp_decode_stage", "hp_decode_bsa_workspace_bytes",
            "hp_decode_bsa", "hp_decode_materialize", "hp_decode_append", "hp_trace_enable", "hp_debug_cut",
-           "hp_cache_workspace_bytes", "hp_cache_commit"]
+           "hp_cache_workspace_bytes", "hp_cache_commit", "hp_select_topk"]
 
 
 def lib():
@@ -161,6 +161,9 @@ def lib():
     L.hp_decode_append.restype = C.c_int
     L.hp_decode_append.argtypes = [C.POINTER(KvView), C.c_void_p, C.c_void_p, C.c_int64,
                                    C.c_void_p, C.c_void_p]
+    L.hp_select_topk.restype = C.c_int
+    L.hp_select_topk.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_int64, C.c_int32,
+                                 C.c_int32, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]
     L.hp_cache_workspace_bytes.restype = C.c_size_t
     L.hp_cache_workspace_bytes.argtypes = [C.c_int32, C.c_int32]
     L.hp_cache_commit.restype = C.c_int

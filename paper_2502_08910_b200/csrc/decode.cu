@@ -225,8 +225,10 @@ decode_stage_kernel(const hp_decode_stage_args a, float* scores, int* tickets, i
     const int chunks_per_cta = 32 * cg;
     const int64_t chunk0 = static_cast<int64_t>(blockIdx.x) * chunks_per_cta;
 
-    if (n_in <= a.keep || cc <= K) {  // identity (pruning.cpp:159-168): keep every chunk
-        if (blockIdx.x == 0) {
+    // identity (pruning.cpp:159-168): keep every chunk — decided here unless this is one
+    // shard of a sequence-sharded stage (scores_out), whose selection is global
+    if (a.scores_out == nullptr && (n_in <= a.keep || cc <= K)) {
+        if (blockIdx.x == 0 && a.sel_out) {
             for (int64_t j = threadIdx.x; j < cc; j += blockDim.x) a.sel_out[static_cast<int64_t>(m) * a.sel_stride + j] = static_cast<int32_t>(j);
             if (threadIdx.x == 0) a.out_count[m] = static_cast<int32_t>(n_in);
         }
@@ -353,7 +355,7 @@ decode_stage_kernel(const hp_decode_stage_args a, float* scores, int* tickets, i
                 const float s = red[h * chunks_per_cta + c];
                 best = (best < s) ? s : best;  // std::max (pruning.cpp:182)
             }
-            scores[static_cast<int64_t>(m) * a.max_chunks + jj] = best;
+            (a.scores_out ? a.scores_out : scores)[static_cast<int64_t>(m) * a.max_chunks + jj] = best;
         }
     }
     trace(10 + lc, 2);
@@ -782,7 +784,8 @@ cudaError_t launch_stage(const hp_decode_stage_args& a, float* scores, int* tick
     const size_t tsmem = static_cast<size_t>(kTopkMaxKeys) * 4 + static_cast<size_t>(kTopkMaxKeys) * 4;  // keys + kept ids
     e = cudaFuncSetAttribute(decode_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(tsmem));
     if (e != cudaSuccess) return e;
-    e = launch_pdl(decode_topk_kernel, dim3(a.n_masks), dim3(kTopkThreads2), tsmem, s, a, scores);
+    e = launch_pdl(decode_topk_kernel, dim3(a.n_masks), dim3(kTopkThreads2), tsmem, s, a,
+                   static_cast<const float*>(a.scores_out ? a.scores_out : scores));
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
@@ -875,6 +878,34 @@ extern "C" int hp_decode_stage(const hp_decode_stage_args* ap, void* stream) {
     if (a.keys.dtype == HP_BF16) e = ext ? launch_stage<bf16_t, true>(a, scores, tickets, s) : launch_stage<bf16_t, false>(a, scores, tickets, s);
     else e = ext ? launch_stage<float, true>(a, scores, tickets, s) : launch_stage<float, false>(a, scores, tickets, s);
     return hph::check_cuda(e, "decode_stage_kernel");
+}
+
+extern "C" int hp_select_topk(const float* scores, int64_t stride, int32_t n_masks, const int32_t* n_in,
+                              int64_t n_in_const, int32_t chunk_size, int32_t keep, int32_t* sel_out,
+                              int32_t sel_stride, int32_t* out_count, void* stream) {
+    if (!scores || !sel_out || !out_count || n_masks <= 0 || stride <= 0)
+        return hph::set_error(HP_INVALID_ARGUMENT, "hp_select_topk: bad arguments");
+    if (chunk_size <= 0 || keep <= 0 || keep % chunk_size)
+        return hph::set_error(HP_INVALID_ARGUMENT, "StageConfig: k must be a positive multiple of l_c");
+    if (sel_stride < keep / chunk_size) return hph::set_error(HP_INVALID_ARGUMENT, "hp_select_topk: sel_stride < k/l_c");
+    if (stride > kTopkMaxKeys)
+        return hph::set_error(HP_INVALID_ARGUMENT, "hp_select_topk: %lld chunks exceed the selection limit %d",
+                              static_cast<long long>(stride), kTopkMaxKeys);
+    hp_decode_stage_args a{};
+    a.chunk_size = chunk_size;
+    a.keep = keep;
+    a.n_masks = n_masks;
+    a.in_count = n_in;
+    a.in_count_const = n_in_const;
+    a.max_chunks = static_cast<int32_t>(stride);
+    a.sel_stride = sel_stride;
+    a.sel_out = sel_out;
+    a.out_count = out_count;
+    const size_t tsmem = static_cast<size_t>(kTopkMaxKeys) * 8;
+    cudaError_t e = cudaFuncSetAttribute(decode_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(tsmem));
+    if (e == cudaSuccess)
+        e = launch_pdl(decode_topk_kernel, dim3(n_masks), dim3(kTopkThreads2), tsmem, static_cast<cudaStream_t>(stream), a, scores);
+    return hph::check_cuda(e, "decode_topk_kernel");
 }
 
 extern "C" size_t hp_decode_bsa_workspace_bytes(int32_t n_q_heads, int32_t max_sel) {
