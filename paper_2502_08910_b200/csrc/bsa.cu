@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(kBsaThreads) bsa_kernel(const hp_bsa_args a, i
     __shared__ float sm_o[4][HC][2 * NC * 32];
     const int d = a.kv.d, half = d >> 1;
     const int split = blockIdx.x, r = blockIdx.y, h0 = blockIdx.z * hc;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31, w = warp_id();
     const int mask = h0 / a.heads_per_mask;
     const int kv = h0 / (a.n_q_heads / a.kv.n_kv);
     const int64_t mr = static_cast<int64_t>(mask) * a.n_rows + r;

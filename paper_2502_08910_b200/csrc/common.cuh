@@ -10,6 +10,12 @@ namespace hpk {
 
 constexpr int kWarp = 32;
 
+// The warp index as a value the compiler can see is warp-uniform (a shuffle from lane
+// 0). Branching on threadIdx.x >> 5 directly makes the compiler treat the branch as
+// possibly divergent inside a warp and turn every shuffle after it into a
+// WARPSYNC.COLLECTIVE emulation loop.
+__device__ __forceinline__ int warp_id() { return __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0); }
+
 __host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
 __host__ __device__ __forceinline__ int64_t max64(int64_t a, int64_t b) { return a > b ? a : b; }
 
@@ -89,7 +95,7 @@ template <int kThreads>
 __device__ __forceinline__ int block_exclusive_scan(int v, int* smem_warp, int* total) {
     static_assert(kThreads % kWarp == 0 && kThreads <= 1024, "block size");
     constexpr int kWarps = kThreads / kWarp;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31, w = warp_id();
     int x = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {

@@ -243,7 +243,7 @@ decode_stage_kernel(const hp_decode_stage_args a, float* scores, int* tickets, i
     float* qs = reinterpret_cast<float*>(smem + static_cast<size_t>(nwarps) * 32 * G::stride);  // [hpm][128]
     uint32_t* qb = reinterpret_cast<uint32_t*>(qs + hpm * kD);                    // [hpm][64] bf16 pairs
     float* red = reinterpret_cast<float*>(qb + hpm * (kD / 2));                   // [hpm][chunks_per_cta]
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31, w = warp_id();
     bool q_safe = true;
     for (int i = threadIdx.x; i < hpm * kD; i += blockDim.x) {
         const float x = a.q[static_cast<int64_t>(m * hpm) * kD + i];
@@ -257,8 +257,11 @@ decode_stage_kernel(const hp_decode_stage_args a, float* scores, int* tickets, i
     if (use_fma) {
         for (int i = threadIdx.x; i < hpm * (kD / 2); i += blockDim.x)
             qb[i] = (__float_as_uint(qs[2 * i]) >> 16) | (__float_as_uint(qs[2 * i + 1]) & 0xffff0000u);
-        __syncthreads();
     }
+    // unconditional barrier: a __syncthreads under a branch makes the compiler treat the
+    // rest of the kernel as possibly warp-divergent (every shuffle becomes a
+    // WARPSYNC.COLLECTIVE emulation loop)
+    __syncthreads();
     if constexpr (EXT) {
         constexpr int half = kD / 2;
         const int64_t qp = rope_q_position(a.rope, a.query_position, a.stream_tokens, cc);
@@ -277,7 +280,16 @@ decode_stage_kernel(const hp_decode_stage_args a, float* scores, int* tickets, i
     const unsigned char* myrow = wstage + lane * G::stride;
     const int swz = lane & (G::bytes / 16 - 1);
 
-    for (int item = w; item < hpm * cg; item += nwarps) {
+    // Items are (head, chunk group) pairs. The trip count is the same for every thread
+    // and a warp past the end redoes the last item (its results are discarded): a
+    // loop bounded by the warp index would read as divergent control flow around the
+    // shuffles below and compile them to WARPSYNC.COLLECTIVE loops.
+    const int n_items = hpm * cg;
+    const int per_warp = (n_items + nwarps - 1) / nwarps;
+    for (int k = 0; k < per_warp; ++k) {
+        const int item_raw = w + k * nwarps;
+        const bool item_ok = item_raw < n_items;
+        const int item = item_ok ? item_raw : n_items - 1;
         const int hh = item % hpm, grp = item / hpm;
         const int qh = m * hpm + hh;
         const int kvh = qh / (a.n_q_heads / a.keys.n_kv);
@@ -315,12 +327,12 @@ decode_stage_kernel(const hp_decode_stage_args a, float* scores, int* tickets, i
         __syncwarp();
         stage_rows<T>(a.keys, kvh, active ? token(0) : -1, wstage, lane,
                       prefetch && active && iters > 0 ? token(mid0 - 1) : -1);
-        if (item == w) trace(10 + lc, 3);
+        if (k == 0) trace(10 + lc, 3);
         if (active) {
             s1 = score(cs1, sn1);
             s2 = same_rot ? s1 : score(cs2, sn2);
         }
-        if (item == w) trace(10 + lc, 4);
+        if (k == 0) trace(10 + lc, 4);
         for (;;) {
             const bool go = active && it < iters && first < last;
             if (!__any_sync(0xffffffffu, go)) break;
@@ -332,16 +344,16 @@ decode_stage_kernel(const hp_decode_stage_args a, float* scores, int* tickets, i
             }
             __syncwarp();
             stage_rows<T>(a.keys, kvh, go ? token(mid - 1) : -1, wstage, lane, pf_r, pf_l);
-            if (item == w && it == 0) trace(10 + lc, 5);
+            if (k == 0 && it == 0) trace(10 + lc, 5);
             if (go) {
                 const float m1 = score(cs1, sn1);
                 const float m2 = same_rot ? m1 : score(cs2, sn2);
                 if (m2 > s1) { first = mid; s1 = m1; s2 = m2; } else { last = mid - 1; }
                 ++it;
             }
-            if (item == w && it == 1) trace(10 + lc, 6);
+            if (k == 0 && it == 1) trace(10 + lc, 6);
         }
-        red[hh * chunks_per_cta + grp * 32 + lane] = s2;
+        if (item_ok) red[hh * chunks_per_cta + grp * 32 + lane] = s2;
         __syncwarp();
     }
     __syncthreads();
@@ -362,6 +374,130 @@ decode_stage_kernel(const hp_decode_stage_args a, float* scores, int* tickets, i
     (void)tickets;
 }
 
+// ------------------------------------------------- all-rows stage kernel (small l_c)
+// For short chunks (l_c <= 32; the 3k preset's stage 3 has l_c = 8) a warp owns
+// 32 / l_c whole chunks: lane i stages row i % l_c of chunk i / l_c (one gather for
+// all the mask's heads, which share one kv head) and computes that row's sequential
+// dot with every head's q (independent accumulators: q is a shared-memory broadcast,
+// the row is read once). Each head's Alg. 3 descent is then replayed on those scores
+// with shuffles inside the chunk's lane group — the same comparisons of the same fp32
+// values, so representatives and scores are exactly the reference's — at one gather
+// latency instead of ceil(log2 l_c) + 1 dependent ones. It reads every row of a chunk
+// (8 here) where the descents touch ~5-7 distinct rows: ~1.2x the distinct bytes at
+// 3k/1M for one dependent round trip instead of four.
+constexpr int kAllRowsWarps = 8;
+constexpr int kAllRowsHeads = 4;  // accumulators per lane (heads per pass)
+
+template <typename T>
+__global__ void __launch_bounds__(kAllRowsWarps * 32)
+decode_stage_allrows_kernel(const hp_decode_stage_args a, float* scores) {
+    pdl_trigger();
+    pdl_wait();
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int cut = dev_cut_point(5);
+    if (cut == 0) return;
+    using G = RowGeom<T>;
+    const int hpm = a.heads_per_mask;
+    const int lc = a.chunk_size;
+    const int m = blockIdx.y;
+    const int64_t n_in = a.in_count ? a.in_count[m] : a.in_count_const;
+    const int64_t cc = (n_in + lc - 1) / lc;
+    const int K = a.keep / lc;
+    if (a.scores_out == nullptr && (n_in <= a.keep || cc <= K)) {  // identity (pruning.cpp:159-168)
+        if (blockIdx.x == 0 && a.sel_out) {
+            for (int64_t j = threadIdx.x; j < cc; j += blockDim.x) a.sel_out[static_cast<int64_t>(m) * a.sel_stride + j] = static_cast<int32_t>(j);
+            if (threadIdx.x == 0) a.out_count[m] = static_cast<int32_t>(n_in);
+        }
+        return;
+    }
+    const int cpw = 32 / lc;  // chunks per warp
+    const int lane = threadIdx.x & 31, w = warp_id();
+    if (static_cast<int64_t>(blockIdx.x) * kAllRowsWarps * cpw >= cc) return;
+    unsigned char* wstage = smem + static_cast<size_t>(w) * 32 * G::stride;
+    float* qs = reinterpret_cast<float*>(smem + static_cast<size_t>(kAllRowsWarps) * 32 * G::stride);
+    uint32_t* qb = reinterpret_cast<uint32_t*>(qs + hpm * kD);
+    bool q_safe = true;
+    for (int i = threadIdx.x; i < hpm * kD; i += blockDim.x) {
+        const float x = a.q[static_cast<int64_t>(m * hpm) * kD + i];
+        qs[i] = x;
+        q_safe &= q_product_safe(x);
+    }
+    const bool use_fma = __syncthreads_and(q_safe) && sizeof(T) == 2 && a.keys_exact != nullptr && *a.keys_exact != 0;
+    if (use_fma) {
+        for (int i = threadIdx.x; i < hpm * (kD / 2); i += blockDim.x)
+            qb[i] = (__float_as_uint(qs[2 * i]) >> 16) | (__float_as_uint(qs[2 * i + 1]) & 0xffff0000u);
+    }
+    __syncthreads();  // unconditional (see decode_stage_kernel)
+    if (cut == 1) return;
+    const int cl = lane / lc, r = lane - cl * lc;  // lane -> (chunk of the warp, row)
+    const int64_t j = (static_cast<int64_t>(blockIdx.x) * kAllRowsWarps + w) * cpw + cl;
+    const bool live = j < cc && cl < cpw;
+    const int kvh = (m * hpm) / (a.n_q_heads / a.keys.n_kv);
+    const int64_t base = j * lc;
+    const int len = live ? static_cast<int>(min64(lc, n_in - base)) : 0;
+    const int64_t tok = r < len ? ref_token(a.in, m, base + r) : -1;
+    if (cut == 2 && tok == 123456789) scores[0] = 0.f;
+    if (cut == 2) return;
+    stage_rows<T>(a.keys, kvh, tok, wstage, lane);
+    if (cut == 3) return;
+    const unsigned char* row = wstage + lane * G::stride;
+    const int swz = lane & (G::bytes / 16 - 1);
+    const int c0 = cl * lc;  // first lane of this chunk
+    int iters = 0;
+    while ((1 << iters) < lc) ++iters;
+    float best = -INFINITY;
+    for (int h0 = 0; h0 < hpm; h0 += kAllRowsHeads) {
+        float acc[kAllRowsHeads];
+#pragma unroll
+        for (int u = 0; u < kAllRowsHeads; ++u) acc[u] = 0.0f;
+        const int nh = min(kAllRowsHeads, hpm - h0);
+        if (use_fma) {
+            const uint4* q4 = reinterpret_cast<const uint4*>(qb + h0 * (kD / 2));
+#pragma unroll 2
+            for (int c = 0; c < 16; ++c) {
+                const uint4 wv = *reinterpret_cast<const uint4*>(row + ((c ^ swz) << 4));
+#pragma unroll
+                for (int u = 0; u < kAllRowsHeads; ++u) {
+                    const uint4 q = q4[min(u, nh - 1) * 16 + c];  // broadcast; u >= nh redoes a head (discarded)
+                    acc[u] = fma_bf16(q.x, wv.x, acc[u], false);
+                    acc[u] = fma_bf16(q.x, wv.x, acc[u], true);
+                    acc[u] = fma_bf16(q.y, wv.y, acc[u], false);
+                    acc[u] = fma_bf16(q.y, wv.y, acc[u], true);
+                    acc[u] = fma_bf16(q.z, wv.z, acc[u], false);
+                    acc[u] = fma_bf16(q.z, wv.z, acc[u], true);
+                    acc[u] = fma_bf16(q.w, wv.w, acc[u], false);
+                    acc[u] = fma_bf16(q.w, wv.w, acc[u], true);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < kAllRowsHeads; ++u)
+                acc[u] = dot_row<T>(row, swz, qs + (h0 + min(u, nh - 1)) * kD);
+        }
+        if (cut == 4 && acc[0] == 1.2345f) scores[0] = 0.f;
+        // Alg. 3 per head on the chunk's row scores (pruning.cpp:69-98): right only on
+        // strict s(mid) > s(first); sigma1 == sigma2 without rotation. ceil(log2 l_c)
+        // rounds for every lane: a short chunk settles early and idles.
+#pragma unroll
+        for (int u = 0; u < kAllRowsHeads; ++u) {
+            const float sc = r < len ? acc[u] : -INFINITY;
+            int first = 1, last = len;
+            float s1 = __shfl_sync(0xffffffffu, sc, c0);
+            for (int it = 0; it < iters; ++it) {
+                const int mid = (first + last + 1) >> 1;
+                const bool go = first < last;
+                const float s2 = __shfl_sync(0xffffffffu, sc, c0 + (go ? mid - 1 : 0));
+                if (go) {
+                    if (s2 > s1) { first = mid; s1 = s2; } else { last = mid - 1; }
+                }
+            }
+            if (u < nh) best = (best < s1) ? s1 : best;  // max over heads (pruning.cpp:182)
+        }
+    }
+    if (cut == 4) return;
+    if (live && r == 0) (a.scores_out ? a.scores_out : scores)[static_cast<int64_t>(m) * a.max_chunks + j] = best;
+}
+
 // ----------------------------------------------------------------- top-k kernel
 // Exact top-(k/l_c) chunk selection for one mask by a 1024-thread CTA: the mask's
 // chunk scores become order keys in shared memory and cta_topk_smem selects; the
@@ -377,6 +513,8 @@ decode_topk_kernel(const hp_decode_stage_args a, const float* scores) {
     pdl_wait();
     extern __shared__ __align__(16) unsigned char tsm[];
     __shared__ TopkShared sh;
+    const int cut = dev_cut_point(3);
+    if (cut == 0) return;
     const int m = blockIdx.x, t = threadIdx.x, nt = blockDim.x;
     const int n_in = a.in_count ? a.in_count[m] : static_cast<int>(a.in_count_const);
     const int lc = a.chunk_size;
@@ -394,7 +532,7 @@ decode_topk_kernel(const hp_decode_stage_args a, const float* scores) {
     trace(3, 0);
     const float* sc = scores + static_cast<int64_t>(m) * a.max_chunks;
     uint32_t* keys = reinterpret_cast<uint32_t*>(tsm);              // [cc]
-    int32_t* ssel = reinterpret_cast<int32_t*>(keys + kTopkMaxKeys);  // [K]
+    int32_t* ssel = reinterpret_cast<int32_t*>(keys + ((a.max_chunks + 3) & ~3));  // [K] after keys[max_chunks]
     {
         constexpr int kPer = kTopkMaxKeys / kTopkThreads2;  // 16 independent loads per thread
         float v[kPer];
@@ -411,12 +549,15 @@ decode_topk_kernel(const hp_decode_stage_args a, const float* scores) {
     }
     __syncthreads();
     trace(3, 1);
+    if (cut == 1) return;
     cta_topk_smem(keys, cc, K, ssel, sh);
     trace(3, 2);
+    if (cut == 2) return;
     for (int i = t; i < K; i += nt) sel[i] = ssel[i];
     const int lastc = ssel[K - 1];
     const int n_out = (K - 1) * lc + min(lc, n_in - lastc * lc);
     if (t == 0) a.out_count[m] = n_out;
+    if (cut == 3) return;
     if (a.list_out) {  // materialize: output position o -> chunk sel[o / lc] -> input list
         for (int o = t; o < n_out; o += nt) {
             const int r = o / lc;
@@ -489,7 +630,7 @@ decode_bsa_kernel(const hp_decode_bsa_args a, float* part, int* tickets, int spl
     unsigned long long* vptr = kptr + kBsaMaxKeys;
     __shared__ int sh_last;
 
-    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const int t = threadIdx.x, lane = t & 31, w = warp_id();
     const int split = blockIdx.x, hg = blockIdx.y;
     const int h0 = hg * HC;
     const int mask = h0 / a.heads_per_mask;
@@ -618,20 +759,30 @@ decode_bsa_kernel(const hp_decode_bsa_args a, float* part, int* tickets, int spl
     trace(2, 3);
     if (cut == 2) return;
     // ---- 3. softmax pieces per head
-    if (w < HC) {
-        float* pr = ps + w * kBsaMaxKeys;
+    {  // every warp runs a head's reduction (warps >= HC redo head w % HC and discard it):
+       // no warp-index branch around the shuffles
+        const int hw = w % HC;
+        const bool mine = w < HC;
+        float* pr = ps + hw * kBsaMaxKeys;
         float mx = -INFINITY;
         for (int j = lane; j < nv; j += 32) mx = fmaxf(mx, pr[j]);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
         float l = 0.f;
-        for (int j = lane; j < kBsaMaxKeys; j += 32) {
-            const float p = (j < nv && mx != -INFINITY) ? expf(pr[j] - mx) : 0.f;
-            pr[j] = p;
-            l += p;
+        float pv[kBsaMaxKeys / 32];
+#pragma unroll
+        for (int i = 0; i < kBsaMaxKeys / 32; ++i) {
+            const int j = i * 32 + lane;
+            pv[i] = (j < nv && mx != -INFINITY) ? expf(pr[j] - mx) : 0.f;
+            l += pv[i];
         }
         l = warp_sum(l);
-        if (lane == 0) { ml[2 * w] = mx; ml[2 * w + 1] = l; }
+        __syncthreads();  // every warp has read its scores before the owners overwrite them
+        if (mine) {
+#pragma unroll
+            for (int i = 0; i < kBsaMaxKeys / 32; ++i) pr[i * 32 + lane] = pv[i];
+            if (lane == 0) { ml[2 * w] = mx; ml[2 * w + 1] = l; }
+        }
     }
     cp_async_wait_all();  // V rows landed
     __syncthreads();
@@ -688,8 +839,9 @@ decode_bsa_kernel(const hp_decode_bsa_args a, float* part, int* tickets, int spl
         mlp[2 * i + 1] = __ldcg(pp + 1);
     }
     __syncthreads();
-    if (w < HC) {
-        const int hh = w;
+    {  // head reductions on every warp (warps >= HC discard theirs), no warp-index branch
+        const int hh = w % HC;
+        const bool mine = w < HC;
         float M = -INFINITY;
         for (int s = lane; s < splits; s += 32)
             if (mlp[2 * (s * HC + hh) + 1] > 0.f) M = fmaxf(M, mlp[2 * (s * HC + hh)]);
@@ -699,11 +851,17 @@ decode_bsa_kernel(const hp_decode_bsa_args a, float* part, int* tickets, int spl
         for (int s = lane; s < splits; s += 32) {
             const float l = mlp[2 * (s * HC + hh) + 1];
             const float f = l > 0.f ? expf(mlp[2 * (s * HC + hh)] - M) : 0.f;
-            mlp[2 * (s * HC + hh)] = f;  // weight replaces m
             L += l * f;
         }
         L = warp_sum(L);
-        if (lane == 0) { ml[2 * hh] = M; ml[2 * hh + 1] = L; }
+        __syncthreads();
+        if (mine) {
+            for (int s = lane; s < splits; s += 32) {
+                const float l = mlp[2 * (s * HC + hh) + 1];
+                mlp[2 * (s * HC + hh)] = l > 0.f ? expf(mlp[2 * (s * HC + hh)] - M) : 0.f;  // weight replaces m
+            }
+            if (lane == 0) { ml[2 * hh] = M; ml[2 * hh + 1] = L; }
+        }
     }
     __syncthreads();
     trace(2, 5);
@@ -770,18 +928,33 @@ cudaError_t launch_stage(const hp_decode_stage_args& a, float* scores, int* tick
     const int nw = threads / 32;
     const size_t smem = static_cast<size_t>(nw) * 32 * G::stride + static_cast<size_t>(hpm) * kD * 6 +
                         static_cast<size_t>(hpm) * 32 * cg * 4;
-    auto kern = decode_stage_kernel<T, EXT>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    dim3 grid((a.max_chunks + 32 * cg - 1) / (32 * cg), a.n_masks);
-    // speculative next-row prefetch only where the stage is latency-bound (few descents)
-    const int64_t lanes = static_cast<int64_t>(a.n_masks) * a.max_chunks * hpm;
-    const int prefetch = lanes <= 65536 ? 1 : 0;
-    e = launch_pdl(kern, grid, dim3(threads), smem, s, a, scores, tickets, cg, prefetch);
+    cudaError_t e;
+    if (!EXT && a.chunk_size <= 8 && 32 % a.chunk_size == 0 && (a.n_q_heads / a.keys.n_kv) % hpm == 0) {
+        // short chunks: gather every row of a chunk at once (decode_stage_allrows_kernel)
+        const size_t smem2 = static_cast<size_t>(kAllRowsWarps) * 32 * G::stride + static_cast<size_t>(hpm) * kD * 6;
+        const int per_cta = kAllRowsWarps * (32 / a.chunk_size);
+        auto k2 = decode_stage_allrows_kernel<T>;
+        e = cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem2));
+        if (e != cudaSuccess) return e;
+        e = launch_pdl(k2, dim3((a.max_chunks + per_cta - 1) / per_cta, a.n_masks), dim3(kAllRowsWarps * 32), smem2, s,
+                       a, scores);
+    } else {
+        auto kern = decode_stage_kernel<T, EXT>;
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        dim3 grid((a.max_chunks + 32 * cg - 1) / (32 * cg), a.n_masks);
+        // speculative next-row prefetch only where the stage is latency-bound (few descents)
+        const int64_t lanes = static_cast<int64_t>(a.n_masks) * a.max_chunks * hpm;
+        const int prefetch = lanes <= 65536 ? 1 : 0;
+        e = launch_pdl(kern, grid, dim3(threads), smem, s, a, scores, tickets, cg, prefetch);
+    }
     if (e != cudaSuccess) return e;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (a.sel_out == nullptr) return cudaSuccess;  // descent only: scores stay in the workspace
-    const size_t tsmem = static_cast<size_t>(kTopkMaxKeys) * 4 + static_cast<size_t>(kTopkMaxKeys) * 4;  // keys + kept ids
+    // keys[max_chunks] + kept ids[K]: sized to the stage so the selection CTAs fit next to
+    // the descent CTAs still draining (they launch early under PDL)
+    const size_t tsmem = static_cast<size_t>((a.max_chunks + 3) & ~3) * 4 +
+                         static_cast<size_t>(std::max(1, a.keep / a.chunk_size)) * 4;
     e = cudaFuncSetAttribute(decode_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(tsmem));
     if (e != cudaSuccess) return e;
     e = launch_pdl(decode_topk_kernel, dim3(a.n_masks), dim3(kTopkThreads2), tsmem, s, a,
@@ -901,7 +1074,7 @@ extern "C" int hp_select_topk(const float* scores, int64_t stride, int32_t n_mas
     a.sel_stride = sel_stride;
     a.sel_out = sel_out;
     a.out_count = out_count;
-    const size_t tsmem = static_cast<size_t>(kTopkMaxKeys) * 8;
+    const size_t tsmem = static_cast<size_t>((stride + 3) & ~3) * 4 + static_cast<size_t>(keep / chunk_size) * 4;
     cudaError_t e = cudaFuncSetAttribute(decode_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(tsmem));
     if (e == cudaSuccess)
         e = launch_pdl(decode_topk_kernel, dim3(n_masks), dim3(kTopkThreads2), tsmem, static_cast<cudaStream_t>(stream), a, scores);

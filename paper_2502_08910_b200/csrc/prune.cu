@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(256) prune_descent_kernel(const hp_stage_args 
         __syncthreads();
     }
 
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31, w = warp_id();
     const int n_warps = blockDim.x >> 5;
     unsigned char* ks = keys + static_cast<size_t>(w) * 32 * g.key_stride;
     unsigned char* myrow = ks + lane * g.key_stride;

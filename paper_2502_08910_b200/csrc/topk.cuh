@@ -9,7 +9,7 @@ namespace hpk {
 // ----------------------------------------------------------------------- top-k
 // Exclusive scan over the CTA for any multiple-of-32 block size.
 __device__ __forceinline__ int block_scan_rt(int v, int* tmp) {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int lane = threadIdx.x & 31, w = warp_id(), nw = blockDim.x >> 5;
     int x = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -48,7 +48,7 @@ struct TopkShared {
 };
 
 __device__ inline void cta_topk_smem(const uint32_t* keys, int cc, int K, int32_t* sel, TopkShared& sh) {
-    const int t = threadIdx.x, nt = blockDim.x, lane = t & 31, w = t >> 5;
+    const int t = threadIdx.x, nt = blockDim.x, lane = t & 31, w = warp_id();
     uint32_t lmin = 0xffffffffu, lmax = 0u;
     for (int j = t; j < cc; j += nt) {
         const uint32_t u = keys[j];

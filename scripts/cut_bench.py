@@ -30,8 +30,20 @@ with torch.cuda.graph(g):
     for _ in range(N):
         layer.run(t, refresh=[False] * 3)
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+kid = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+stage_of = {5: 2, 3: int(sys.argv[3]) if len(sys.argv) > 3 else 0}
+if kid == 3:  # a stage's top-k kernel (descent + top-k launched; the cut applies to top-k)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(N):
+            layer.run_stage(t, stage_of[3])
+if kid == 5:  # stage-3 descent (all-rows kernel)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(N):
+            layer.run_stage(t, 2, select=False)
 for cut in [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "0,5,6,7,1,2,3,4,-1").split(",")]:
-    _capi.check(L.hp_debug_cut(2, cut))
+    _capi.check(L.hp_debug_cut(kid, cut))
     ts = []
     for _ in range(10):
         flush.zero_()
@@ -39,4 +51,4 @@ for cut in [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "0,5,6,7,1,2,
         a.record(); g.replay(); b.record(); torch.cuda.synchronize()
         ts.append(a.elapsed_time(b) * 1e3 / N)
     ts.sort()
-    print(f"bsa cut at {cut:2d}: {ts[len(ts)//2]:7.2f} us per launch (graph of {N})")
+    print(f"kernel {kid} cut at {cut:2d}: {ts[len(ts)//2]:7.2f} us per launch (graph of {N})")
