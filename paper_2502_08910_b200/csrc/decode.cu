@@ -374,6 +374,112 @@ decode_stage_kernel(const hp_decode_stage_args a, float* scores, int* tickets, i
     (void)tickets;
 }
 
+// ------------------------------------------------------ one-wave stage kernel (big stages)
+// The long-chunk descents (stage 1: 4,091 chunks x 32 q-heads at 1M) need every warp
+// resident at once: a warp of 32 descents stages 32 rows (8 KB), and a second wave of
+// CTAs would run the whole 9-step dependent chain again at low occupancy. Here a CTA
+// is 7 warps (56 KB of staging, nothing else in shared memory): 4 CTAs fill an SM's
+// 228 KB, 148 x 4 x 7 = 4,144 warps >= 4,096 items. Each warp is one (mask, chunk
+// group, head) item; q is read through L1 (a broadcast), and each warp writes its
+// head's representative scores to [mask][head][chunk] — the selection takes the max
+// over heads in head order, as the reference does.
+constexpr int kWideWarps = 7;
+
+template <typename T>
+__global__ void __launch_bounds__(kWideWarps * 32, 4)
+decode_stage_wide_kernel(const hp_decode_stage_args a, float* hscores, int groups) {
+    pdl_trigger();
+    pdl_wait();
+    extern __shared__ __align__(128) unsigned char smem[];
+    using G = RowGeom<T>;
+    const int hpm = a.heads_per_mask;
+    const int lc = a.chunk_size;
+    const int lane = threadIdx.x & 31, w = warp_id();
+    const int per_mask = groups * hpm;
+    const int item_raw = blockIdx.x * kWideWarps + w;
+    const bool item_ok = item_raw < a.n_masks * per_mask;
+    const int item = item_ok ? item_raw : 0;
+    const int m = item / per_mask, rem = item - m * per_mask;
+    const int g = rem / hpm, hh = rem - g * hpm;  // the heads of a chunk group are adjacent items
+    const int64_t n_in = a.in_count ? a.in_count[m] : a.in_count_const;
+    const int64_t cc = (n_in + lc - 1) / lc;
+    const int K = a.keep / lc;
+    // identity stages need no scores (the selection keeps every chunk)
+    const bool run = item_ok && !(n_in <= a.keep || cc <= K) && static_cast<int64_t>(g) * 32 < cc;
+    const int qh = m * hpm + hh;
+    const int kvh = qh / (a.n_q_heads / a.keys.n_kv);
+    const float* qrow = a.q + static_cast<int64_t>(qh) * kD;
+    // FFMA when every product is exact (bf16-exact q, keys certified), FMUL+FADD otherwise
+    bool q_safe = true;
+#pragma unroll
+    for (int i = 0; i < kD / 32; ++i) q_safe &= q_product_safe(__ldg(qrow + i * 32 + lane));
+    const bool use_fma = __all_sync(0xffffffffu, q_safe) && sizeof(T) == 2 && a.keys_exact != nullptr &&
+                         *a.keys_exact != 0;
+    unsigned char* wstage = smem + static_cast<size_t>(w) * 32 * G::stride;
+    const unsigned char* myrow = wstage + lane * G::stride;
+    const int swz = lane & (G::bytes / 16 - 1);
+    const int64_t j = static_cast<int64_t>(g) * 32 + lane;
+    const bool active = run && j < cc;
+    const int64_t base = j * lc;
+    const int len = active ? static_cast<int>(min64(lc, n_in - base)) : 0;
+    int64_t t_first = 0;
+    bool contiguous = true;
+    if (active) {
+        t_first = ref_token(a.in, m, base);
+        if (len > 1) contiguous = ref_token(a.in, m, base + len - 1) - t_first == len - 1;
+    }
+    auto token = [&](int i) -> int64_t { return contiguous ? t_first + i : ref_token(a.in, m, base + i); };
+    auto score = [&]() -> float {
+        // q through L1: every lane reads the same address (one wavefront per load)
+        const float4* q4 = reinterpret_cast<const float4*>(qrow);
+        float acc = 0.0f;
+        if constexpr (sizeof(T) == 2) {
+#pragma unroll 4
+            for (int c = 0; c < 16; ++c) {
+                const uint4 wv = *reinterpret_cast<const uint4*>(myrow + ((c ^ swz) << 4));
+                const float4 qa = __ldg(q4 + 2 * c), qb = __ldg(q4 + 2 * c + 1);
+                if (use_fma) {
+                    acc = __fmaf_rn(qa.x, bf16_lo(wv.x), acc); acc = __fmaf_rn(qa.y, bf16_hi(wv.x), acc);
+                    acc = __fmaf_rn(qa.z, bf16_lo(wv.y), acc); acc = __fmaf_rn(qa.w, bf16_hi(wv.y), acc);
+                    acc = __fmaf_rn(qb.x, bf16_lo(wv.z), acc); acc = __fmaf_rn(qb.y, bf16_hi(wv.z), acc);
+                    acc = __fmaf_rn(qb.z, bf16_lo(wv.w), acc); acc = __fmaf_rn(qb.w, bf16_hi(wv.w), acc);
+                } else {
+                    acc = __fadd_rn(acc, __fmul_rn(qa.x, bf16_lo(wv.x))); acc = __fadd_rn(acc, __fmul_rn(qa.y, bf16_hi(wv.x)));
+                    acc = __fadd_rn(acc, __fmul_rn(qa.z, bf16_lo(wv.y))); acc = __fadd_rn(acc, __fmul_rn(qa.w, bf16_hi(wv.y)));
+                    acc = __fadd_rn(acc, __fmul_rn(qb.x, bf16_lo(wv.z))); acc = __fadd_rn(acc, __fmul_rn(qb.y, bf16_hi(wv.z)));
+                    acc = __fadd_rn(acc, __fmul_rn(qb.z, bf16_lo(wv.w))); acc = __fadd_rn(acc, __fmul_rn(qb.w, bf16_hi(wv.w)));
+                }
+            }
+        } else {
+#pragma unroll 4
+            for (int c = 0; c < 32; ++c) {
+                const float4 wv = *reinterpret_cast<const float4*>(myrow + ((c ^ swz) << 4));
+                const float4 qa = __ldg(q4 + c);
+                acc = __fadd_rn(acc, __fmul_rn(qa.x, wv.x)); acc = __fadd_rn(acc, __fmul_rn(qa.y, wv.y));
+                acc = __fadd_rn(acc, __fmul_rn(qa.z, wv.z)); acc = __fadd_rn(acc, __fmul_rn(qa.w, wv.w));
+            }
+        }
+        return acc;
+    };
+    int first = 1, last = len, it = 0, iters = 0;
+    while ((1 << iters) < len) ++iters;
+    float s1 = 0.f;
+    stage_rows<T>(a.keys, kvh, active ? token(0) : -1, wstage, lane);
+    if (active) s1 = score();
+    for (;;) {
+        const bool go = active && it < iters && first < last;
+        if (!__any_sync(0xffffffffu, go)) break;
+        const int mid = (first + last + 1) >> 1;
+        stage_rows<T>(a.keys, kvh, go ? token(mid - 1) : -1, wstage, lane);
+        if (go) {
+            const float m2 = score();
+            if (m2 > s1) { first = mid; s1 = m2; } else { last = mid - 1; }
+            ++it;
+        }
+    }
+    if (active) hscores[(static_cast<int64_t>(m) * hpm + hh) * a.max_chunks + j] = s1;
+}
+
 // ------------------------------------------------- all-rows stage kernel (small l_c)
 // For short chunks (l_c <= 32; the 3k preset's stage 3 has l_c = 8) a warp owns
 // 32 / l_c whole chunks: lane i stages row i % l_c of chunk i / l_c (one gather for
@@ -507,8 +613,32 @@ decode_stage_allrows_kernel(const hp_decode_stage_args a, float* scores) {
 constexpr int kTopkThreads2 = 1024;
 constexpr int kTopkMaxKeys = 16384;
 
+template <int HP>
+__device__ __forceinline__ void load_head_max(const float* sc, int stride, int cc, uint32_t* keys, int hp = HP) {
+    constexpr int kPer = 4;  // chunks per thread per round (4,096 chunks = one round at 1,024 threads)
+    const int t = threadIdx.x, nt = blockDim.x;
+    for (int j0 = 0; j0 < cc; j0 += kPer * nt) {
+        float v[kPer][HP];
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const int j = j0 + k * nt + t;
+#pragma unroll
+            for (int h = 0; h < HP; ++h)
+                v[k][h] = (j < cc && h < hp) ? __ldcg(sc + static_cast<int64_t>(h) * stride + j) : -INFINITY;
+        }
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const int j = j0 + k * nt + t;
+            float best = -INFINITY;
+#pragma unroll
+            for (int h = 0; h < HP; ++h) best = (best < v[k][h]) ? v[k][h] : best;
+            if (j < cc) keys[j] = order_key(best);
+        }
+    }
+}
+
 __global__ void __launch_bounds__(kTopkThreads2)
-decode_topk_kernel(const hp_decode_stage_args a, const float* scores) {
+decode_topk_kernel(const hp_decode_stage_args a, const float* scores, int head_planes) {
     pdl_trigger();
     pdl_wait();
     extern __shared__ __align__(16) unsigned char tsm[];
@@ -530,10 +660,10 @@ decode_topk_kernel(const hp_decode_stage_args a, const float* scores) {
         return;
     }
     trace(3, 0);
-    const float* sc = scores + static_cast<int64_t>(m) * a.max_chunks;
     uint32_t* keys = reinterpret_cast<uint32_t*>(tsm);              // [cc]
     int32_t* ssel = reinterpret_cast<int32_t*>(keys + ((a.max_chunks + 3) & ~3));  // [K] after keys[max_chunks]
-    {
+    if (head_planes <= 1) {
+        const float* sc = scores + static_cast<int64_t>(m) * a.max_chunks;
         constexpr int kPer = kTopkMaxKeys / kTopkThreads2;  // 16 independent loads per thread
         float v[kPer];
 #pragma unroll
@@ -545,6 +675,17 @@ decode_topk_kernel(const hp_decode_stage_args a, const float* scores) {
         for (int k = 0; k < kPer; ++k) {
             const int j = k * nt + t;
             if (j < cc) keys[j] = order_key(v[k]);
+        }
+    } else {
+        // per-head representative scores [m][head][chunk]: chunk score = max over the
+        // mask's heads in head order (pruning.cpp:176-184, std::max from -inf); every
+        // load of the thread's chunks x heads is issued before the first use
+        const float* sc = scores + static_cast<int64_t>(m) * head_planes * a.max_chunks;
+        switch (head_planes) {
+            case 2: load_head_max<2>(sc, a.max_chunks, cc, keys); break;
+            case 3: load_head_max<3>(sc, a.max_chunks, cc, keys); break;
+            case 4: load_head_max<4>(sc, a.max_chunks, cc, keys); break;
+            default: load_head_max<8>(sc, a.max_chunks, cc, keys, head_planes); break;
         }
     }
     __syncthreads();
@@ -929,7 +1070,22 @@ cudaError_t launch_stage(const hp_decode_stage_args& a, float* scores, int* tick
     const size_t smem = static_cast<size_t>(nw) * 32 * G::stride + static_cast<size_t>(hpm) * kD * 6 +
                         static_cast<size_t>(hpm) * 32 * cg * 4;
     cudaError_t e;
-    if (!EXT && a.chunk_size <= 8 && 32 % a.chunk_size == 0 && (a.n_q_heads / a.keys.n_kv) % hpm == 0) {
+    int head_planes = 1;
+    const int groups = (a.max_chunks + 31) / 32;
+    const int64_t wide_items = static_cast<int64_t>(a.n_masks) * groups * hpm;
+    if (!EXT && a.scores_out == nullptr && a.chunk_size > 8 && hpm <= 8 &&
+        align_up(static_cast<size_t>(a.n_masks) * 4, 256) + static_cast<size_t>(a.n_masks) * hpm * a.max_chunks * 4 <=
+            a.workspace_bytes &&
+        wide_items > 2048) {
+        // big stage: one wave of 7-warp CTAs, per-head scores (decode_stage_wide_kernel)
+        const size_t smem3 = static_cast<size_t>(kWideWarps) * 32 * G::stride;
+        auto k3 = decode_stage_wide_kernel<T>;
+        e = cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem3));
+        if (e != cudaSuccess) return e;
+        head_planes = hpm;
+        e = launch_pdl(k3, dim3(static_cast<unsigned>((wide_items + kWideWarps - 1) / kWideWarps)), dim3(kWideWarps * 32),
+                       smem3, s, a, scores, groups);
+    } else if (!EXT && a.chunk_size <= 8 && 32 % a.chunk_size == 0 && (a.n_q_heads / a.keys.n_kv) % hpm == 0) {
         // short chunks: gather every row of a chunk at once (decode_stage_allrows_kernel)
         const size_t smem2 = static_cast<size_t>(kAllRowsWarps) * 32 * G::stride + static_cast<size_t>(hpm) * kD * 6;
         const int per_cta = kAllRowsWarps * (32 / a.chunk_size);
@@ -958,7 +1114,7 @@ cudaError_t launch_stage(const hp_decode_stage_args& a, float* scores, int* tick
     e = cudaFuncSetAttribute(decode_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(tsmem));
     if (e != cudaSuccess) return e;
     e = launch_pdl(decode_topk_kernel, dim3(a.n_masks), dim3(kTopkThreads2), tsmem, s, a,
-                   static_cast<const float*>(a.scores_out ? a.scores_out : scores));
+                   static_cast<const float*>(a.scores_out ? a.scores_out : scores), head_planes);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
@@ -1008,9 +1164,12 @@ extern "C" int hp_trace_enable(unsigned long long* buf, int kernel_id) {
     return hph::check_cuda(cudaMemcpyToSymbol(g_trace_kernel, &kernel_id, sizeof(int)), "hp_trace_enable");
 }
 
+// tickets, then chunk scores with room for up to kWideHeadPlanes per-head planes (the
+// one-wave kernel keeps every head's representative score; the selection maxes them)
+constexpr int kWideHeadPlanes = 8;
 extern "C" size_t hp_decode_stage_workspace_bytes(int32_t n_masks, int32_t max_chunks) {
-    return align_up(static_cast<size_t>(n_masks) * 4, 256) +             // tickets
-           align_up(static_cast<size_t>(n_masks) * std::max(1, max_chunks) * 4, 256);  // scores
+    return align_up(static_cast<size_t>(n_masks) * 4, 256) +
+           align_up(static_cast<size_t>(n_masks) * kWideHeadPlanes * std::max(1, max_chunks) * 4, 256);
 }
 
 extern "C" int hp_decode_stage(const hp_decode_stage_args* ap, void* stream) {
@@ -1077,7 +1236,8 @@ extern "C" int hp_select_topk(const float* scores, int64_t stride, int32_t n_mas
     const size_t tsmem = static_cast<size_t>((stride + 3) & ~3) * 4 + static_cast<size_t>(keep / chunk_size) * 4;
     cudaError_t e = cudaFuncSetAttribute(decode_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(tsmem));
     if (e == cudaSuccess)
-        e = launch_pdl(decode_topk_kernel, dim3(n_masks), dim3(kTopkThreads2), tsmem, static_cast<cudaStream_t>(stream), a, scores);
+        e = launch_pdl(decode_topk_kernel, dim3(n_masks), dim3(kTopkThreads2), tsmem, static_cast<cudaStream_t>(stream), a,
+                       scores, 1);
     return hph::check_cuda(e, "decode_topk_kernel");
 }
 
