@@ -384,7 +384,7 @@ def main():
             "bsa_only_us": bsa_us / world,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "decode_stage_kernel<bf16> (stage-1 descent, 8 KV groups)",
+                         "kernel": "decode_stage_wide_kernel<bf16> (stage-1 descent, 8 KV groups)",
                          "kernel_us": s1_us, "algorithmic_bytes": alg_bytes,
                          "distinct_key_rows": rows, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"},
             "cpu_baseline": cpu,
