@@ -176,6 +176,38 @@ size_t hp_bsa_workspace_bytes(int32_t n_q_heads, int32_t n_rows, int32_t max_sel
 int hp_bsa(const hp_bsa_args* args, void* stream);
 
 /* ------------------------------------------------------------------------ *
+ * Prefill block-sparse attention on the tensor cores (tcgen05 + TMEM): each
+ * query block's rows x its union of selected keys as 128 x 128 MMA tiles, the
+ * per-row selection (selected_indices, sparse_attention.cpp:95-112) applied as a
+ * mask on the scores, online softmax, O accumulated in TMEM. Replaces
+ * block_sparse_attention (sparse_attention.cpp:114-145) for bf16 K/V, d = 128,
+ * extension off; Q and P enter the tensor cores as bf16 (bf16 tolerance).
+ * ------------------------------------------------------------------------ */
+typedef struct hp_bsa_prefill_args {
+    int32_t n_q_heads;
+    int32_t heads_per_mask;      /* q-heads pooled into one mask (one KV group)          */
+    int32_t n_rows;              /* T_q                                                 */
+    int32_t block_size;          /* mask block size b_q (divides 128)                   */
+    const float* q;              /* [n_q_heads][n_rows][128] fp32                       */
+    int64_t query_offset;        /* T_kv - T_q                                          */
+    const int32_t* mask_list;    /* [n_masks][n_mask_blocks][mask_stride] middle indices */
+    const int32_t* mask_count;   /* [n_masks][n_mask_blocks]                            */
+    int64_t mask_stride;
+    int32_t n_mask_blocks;
+    int32_t max_mask;            /* upper bound on mask_count                           */
+    int32_t sink_tokens;
+    int32_t stream_tokens;
+    float* out;                  /* [n_q_heads][n_rows][128] fp32                       */
+    hp_kv_view kv;               /* bf16, d = 128                                       */
+} hp_bsa_prefill_args;
+
+size_t hp_bsa_prefill_smem_bytes(int32_t max_union);
+/* Developer instrumentation: the prefill kernel's thread 0 writes progress codes to
+ * this (device-mapped pinned host) word; NULL disables. */
+int hp_debug_prefill_progress(int* mapped_word);
+int hp_bsa_prefill(const hp_bsa_prefill_args* args, void* stream);
+
+/* ------------------------------------------------------------------------ *
  * Fused decode path (one query row per q-head, d = 128): the per-layer body of
  * DecodeEngine::step (decode.cpp:225-273) as 1 kernel per stage + 1 BSA kernel.
  * Stage outputs stay implicit between kernels: a stage emits only its kept

@@ -97,6 +97,14 @@ class DecodeBsaArgs(C.Structure):
                 ("workspace_bytes", C.c_size_t), ("kv", KvView), ("rope", RopeCtx)]
 
 
+class BsaPrefillArgs(C.Structure):
+    _fields_ = [("n_q_heads", C.c_int32), ("heads_per_mask", C.c_int32), ("n_rows", C.c_int32),
+                ("block_size", C.c_int32), ("q", C.c_void_p), ("query_offset", C.c_int64),
+                ("mask_list", C.c_void_p), ("mask_count", C.c_void_p), ("mask_stride", C.c_int64),
+                ("n_mask_blocks", C.c_int32), ("max_mask", C.c_int32), ("sink_tokens", C.c_int32),
+                ("stream_tokens", C.c_int32), ("out", C.c_void_p), ("kv", KvView)]
+
+
 class PageCache(C.Structure):
     _fields_ = [("k_slots", C.c_void_p), ("v_slots", C.c_void_p), ("k_host", C.c_void_p),
                 ("v_host", C.c_void_p), ("page_table", C.c_void_p), ("slot_page", C.c_void_p),
@@ -113,7 +121,8 @@ EXPORTS = ["hp_last_error", "hp_version", "hp_device_available", "hp_build_rope_
            "hp_selected_indices", "hp_bsa_workspace_bytes", "hp_bsa", "hp_lse_merge",
            "hp_decode_stage_workspace_bytes", "hp_decode_stage", "hp_decode_bsa_workspace_bytes",
            "hp_decode_bsa", "hp_decode_materialize", "hp_decode_append", "hp_trace_enable", "hp_debug_cut",
-           "hp_cache_workspace_bytes", "hp_cache_commit", "hp_select_topk"]
+           "hp_cache_workspace_bytes", "hp_cache_commit", "hp_select_topk",
+           "hp_bsa_prefill_smem_bytes", "hp_bsa_prefill", "hp_debug_prefill_progress"]
 
 
 def lib():
@@ -161,6 +170,10 @@ def lib():
     L.hp_decode_append.restype = C.c_int
     L.hp_decode_append.argtypes = [C.POINTER(KvView), C.c_void_p, C.c_void_p, C.c_int64,
                                    C.c_void_p, C.c_void_p]
+    L.hp_bsa_prefill_smem_bytes.restype = C.c_size_t
+    L.hp_bsa_prefill_smem_bytes.argtypes = [C.c_int32]
+    L.hp_bsa_prefill.restype = C.c_int
+    L.hp_bsa_prefill.argtypes = [C.POINTER(BsaPrefillArgs), C.c_void_p]
     L.hp_select_topk.restype = C.c_int
     L.hp_select_topk.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_int64, C.c_int32,
                                  C.c_int32, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]

@@ -1,0 +1,421 @@
+// Prefill block-sparse attention on the 5th-generation tensor cores (tcgen05 + TMEM).
+//
+// Replaces block_sparse_attention (reference proj/src/sparse_attention.cpp:114-145):
+// every query row r attends to its selected set — sinks [0, min(n_sink, pos+1)), the
+// mask of its query block inside [sink_end, stream_begin), and the stream window
+// [stream_begin, pos] — with scale 1/sqrt(d) and a softmax over that set.
+//
+// A CTA owns one query block (b_q rows) for the 128 / b_q q-heads of one KV group that
+// fill a 128-row MMA tile, so every key tile is shared by those heads (GQA). The
+// block's union key list (sinks ∪ mask ∪ the block's stream span, each token once,
+// flagged with mask membership) is built in shared memory; per row, key u counts iff
+//   u <= pos  &&  (u < n_sink  ||  u in mask  ||  u >= stream_begin(pos))
+// which is exactly selected_indices (sparse_attention.cpp:95-112) for that row.
+// Per 128-key tile:
+//   1. gather the K and V rows (16-byte cp.async through the page table) into the
+//      canonical no-swizzle UMMA layouts (K K-major, V MN-major), bf16;
+//   2. one thread issues S = Q K^T as 8 x tcgen05.mma (M=128, N=128, K=16) into TMEM;
+//   3. each thread owns one row: tcgen05.ld of its S row, causal/selection mask,
+//      online-softmax update, P (bf16) to shared memory, O rescaled in TMEM
+//      (tcgen05.ld / tcgen05.st);
+//   4. O += P V as 8 x tcgen05.mma into the TMEM accumulator.
+// MMA completion is tracked with tcgen05.commit -> mbarrier. The tile contraction is
+// bf16 x bf16 -> fp32 (Q and P rounded to bf16): the stated bf16 tolerance applies.
+#include <cstdint>
+
+#include "common.cuh"
+
+using namespace hpk;
+
+namespace {
+
+constexpr int kTM = 128;       // query rows per MMA tile (TMEM lanes)
+constexpr int kTN = 128;       // keys per tile
+constexpr int kHD = 128;       // head dim
+constexpr int kThreads = 128;  // one thread per query row
+constexpr uint32_t kTmemCols = 256;  // S [0,128) + O [128,256)
+
+// canonical no-swizzle layouts, byte offsets (8 x 16 B core matrices)
+// K-major [rows][K]: (r/8)*2048 + (k/8)*128 + (r%8)*16 + (k%8)*2  -> SBO 2048, LBO 128
+__device__ __forceinline__ uint32_t kmajor_off(int r, int k) {
+    return static_cast<uint32_t>((r >> 3) * 2048 + (k >> 3) * 128 + (r & 7) * 16 + (k & 7) * 2);
+}
+// MN-major [K rows][MN]: (mn/8)*128 + (k/8)*2048 + (k%8)*16 + (mn%8)*2 -> SBO 128, LBO 2048
+__device__ __forceinline__ uint32_t mnmajor_off(int k, int mn) {
+    return static_cast<uint32_t>((mn >> 3) * 128 + (k >> 3) * 2048 + (k & 7) * 16 + (mn & 7) * 2);
+}
+
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+    d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
+    d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
+    d |= static_cast<uint64_t>(1) << 46;  // descriptor version (Blackwell)
+    return d;                              // base offset 0, swizzle none
+}
+
+// kind::f16 instruction descriptor: bf16 A/B, fp32 C, M x N, major modes
+__host__ __device__ constexpr uint32_t instr_desc(int M, int N, int a_mn_major, int b_mn_major) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(a_mn_major) << 15) |
+           (static_cast<uint32_t>(b_mn_major) << 16) | (static_cast<uint32_t>(N >> 3) << 17) |
+           (static_cast<uint32_t>(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float* v) {
+    uint32_t r[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(v[i]);
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+        "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
+        "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
+        "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+        : "memory");
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+
+// mbarrier wait with a bound: a protocol error traps (a CUDA error) instead of hanging
+__device__ __forceinline__ void mbar_wait_bounded(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    for (uint32_t spin = 0; spin < (1u << 24); ++spin) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+        if (done) return;
+    }
+    __trap();
+}
+
+// dev: progress codes written by thread 0 to a (mapped host) word, to locate a stall
+__device__ volatile int* g_pf_progress = nullptr;
+__device__ __forceinline__ void progress(int code) {
+    if (threadIdx.x == 0 && g_pf_progress) {
+        *g_pf_progress = code;
+        __threadfence_system();
+    }
+}
+
+struct PrefillSmem {
+    static constexpr uint32_t q_off = 0;
+    static constexpr uint32_t k_off = q_off + kTM * kHD * 2;
+    static constexpr uint32_t v_off = k_off + kTN * kHD * 2;
+    static constexpr uint32_t p_off = v_off + kTN * kHD * 2;
+    static constexpr uint32_t u_off = p_off + kTM * kTN * 2;  // union list (int32, bit 31 = in mask)
+};
+
+__global__ void __launch_bounds__(kThreads, 1) bsa_prefill_tc_kernel(const hp_bsa_prefill_args a, int max_union) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bar_s, bar_o;
+    __shared__ uint32_t tmem_base_sh;
+    __shared__ int sh_counts[4];
+    using S = PrefillSmem;
+    const int t = threadIdx.x, lane = t & 31, w = warp_id();
+    const int bs = a.block_size;
+    const int hpt = kTM / bs;  // heads per tile
+    const int b = blockIdx.x, m = blockIdx.y, hp = blockIdx.z;
+    const int hpm = a.heads_per_mask;
+    const int kvh = (m * hpm) / (a.n_q_heads / a.kv.n_kv);
+    const int row0 = b * bs;
+    const int rows_here = min(bs, a.n_rows - row0);
+    const int64_t pos_first = a.query_offset + row0;
+    const int64_t pos_last = pos_first + rows_here - 1;
+    const int64_t sink = a.sink_tokens;
+    auto stream_begin = [&](int64_t pos) {
+        const int64_t se = min64(sink, pos + 1);
+        const int64_t sb = pos + 1 > a.stream_tokens ? pos + 1 - a.stream_tokens : 0;
+        return max64(sb, se);
+    };
+    const int64_t sbf = stream_begin(pos_first);
+    const int64_t s0 = min64(sink, pos_last + 1);  // sinks of the union
+    const int32_t* mlist = a.mask_list + (static_cast<int64_t>(m) * a.n_mask_blocks + b) * a.mask_stride;
+    const int mcount = a.mask_count[static_cast<int64_t>(m) * a.n_mask_blocks + b];
+
+    progress(1);
+    // ---- TMEM + barriers
+    if (w == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
+                     "r"(kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (t == 0) {
+        mbar_init(&bar_s, 1);
+        mbar_init(&bar_o, 1);
+    }
+    // ---- union key list: sinks, mask entries below sbf, then the stream span [max(sbf, s0), pos_last]
+    int32_t* uni = reinterpret_cast<int32_t*>(smem + S::u_off);
+    if (t == 0) {
+        int lo = 0, hi = mcount;  // first mask entry >= sbf
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (mlist[mid] < sbf) lo = mid + 1; else hi = mid;
+        }
+        int msink = 0;  // mask entries < s0 are sinks already (middle lists start at n_sink)
+        while (msink < lo && mlist[msink] < s0) ++msink;
+        sh_counts[0] = msink;
+        sh_counts[1] = lo;
+        sh_counts[2] = static_cast<int>(max64(0, pos_last + 1 - max64(sbf, s0)));
+    }
+    progress(2);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base_sh;
+    progress(3);
+    const int msink = sh_counts[0], mmid = sh_counts[1], nstream = sh_counts[2];
+    const int nmid = mmid - msink;
+    const int64_t st0 = max64(sbf, s0);
+    const int U = static_cast<int>(s0) + nmid + nstream;
+    for (int i = t; i < U; i += kThreads) {
+        int32_t v;
+        if (i < s0) v = i;
+        else if (i < s0 + nmid) v = mlist[msink + i - s0] | static_cast<int32_t>(0x80000000u);
+        else v = static_cast<int32_t>(st0 + (i - s0 - nmid));
+        uni[i] = v;
+    }
+    __syncthreads();
+    // mask entries inside the stream span: flag them (a row whose own stream window starts
+    // later still selects them through its mask)
+    for (int i = mmid + t; i < mcount; i += kThreads) {
+        const int64_t u = mlist[i];
+        if (u >= st0 && u <= pos_last) uni[s0 + nmid + (u - st0)] |= static_cast<int32_t>(0x80000000u);
+    }
+    // ---- Q tile (bf16, K-major): tile row i = head (i / bs) of the pair, block row (i % bs)
+    {
+        const int i = t;
+        const int hh = hp * hpt + i / bs, r = i % bs;
+        const bool ok = r < rows_here;
+        const float* qr = a.q + (static_cast<int64_t>(m * hpm + hh) * a.n_rows + row0 + r) * kHD;
+        unsigned char* qs = smem + S::q_off;
+        for (int c = 0; c < kHD / 8; ++c) {
+            uint4 pk = make_uint4(0, 0, 0, 0);
+            if (ok) {
+                const float4 x0 = reinterpret_cast<const float4*>(qr)[2 * c];
+                const float4 x1 = reinterpret_cast<const float4*>(qr)[2 * c + 1];
+                pk = make_uint4(pack_bf16(x0.x, x0.y), pack_bf16(x0.z, x0.w), pack_bf16(x1.x, x1.y), pack_bf16(x1.z, x1.w));
+            }
+            *reinterpret_cast<uint4*>(qs + kmajor_off(i, c * 8)) = pk;
+        }
+    }
+    const int my_i = t;
+    const int my_r = my_i % bs;
+    const bool my_ok = my_r < rows_here;
+    const int64_t my_pos = pos_first + (my_ok ? my_r : rows_here - 1);
+    const int64_t my_sb = stream_begin(my_pos);
+    const float scale = 1.0f / sqrtf(static_cast<float>(kHD));
+    float run_m = -INFINITY, run_l = 0.f;
+    const uint32_t lane_base = static_cast<uint32_t>(w * 32) << 16;
+    const uint32_t tS = tmem + lane_base;          // S columns [0, 128)
+    const uint32_t tO = tmem + lane_base + 128;    // O columns [128, 256)
+    const uint32_t idesc_qk = instr_desc(kTM, kTN, 0, 0);
+    const uint32_t idesc_pv = instr_desc(kTM, kHD, 0, 1);
+    const uint32_t sbase = smem_u32(smem);
+    const int n_tiles = (U + kTN - 1) / kTN;
+    for (int tile = 0; tile < n_tiles; ++tile) {
+        // 0. the previous P.V has finished reading P, V (and K via program order)
+        if (tile > 0) {
+            mbar_wait_bounded(&bar_o, (tile - 1) & 1);
+            tc_fence_after();
+        }
+        // 1. gather this tile's K and V rows (thread = key)
+        {
+            const int j = t;
+            const int ui = tile * kTN + j;
+            unsigned char* ks = smem + S::k_off;
+            unsigned char* vs = smem + S::v_off;
+            if (ui < U) {
+                const int64_t tok = uni[ui] & 0x7fffffff;
+                const char* kp = kv_row_ptr(a.kv, a.kv.k_pool, a.kv.k_host, kvh, tok, 2);
+                const char* vp = kv_row_ptr(a.kv, a.kv.v_pool, a.kv.v_host, kvh, tok, 2);
+#pragma unroll
+                for (int c = 0; c < kHD / 8; ++c) {
+                    cp_async16(ks + kmajor_off(j, c * 8), kp + c * 16);
+                    cp_async16(vs + mnmajor_off(j, c * 8), vp + c * 16);
+                }
+            } else {
+#pragma unroll
+                for (int c = 0; c < kHD / 8; ++c) {
+                    *reinterpret_cast<uint4*>(ks + kmajor_off(j, c * 8)) = make_uint4(0, 0, 0, 0);
+                    *reinterpret_cast<uint4*>(vs + mnmajor_off(j, c * 8)) = make_uint4(0, 0, 0, 0);
+                }
+            }
+        }
+        cp_async_wait_all();
+        fence_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        progress(10 + tile * 10);
+        // 2. S = Q K^T
+        if (t == 0) {
+            tc_fence_after();
+#pragma unroll
+            for (int k = 0; k < kHD / 16; ++k) {
+                const uint64_t da = smem_desc(sbase + S::q_off + k * 256, 128, 2048);
+                const uint64_t db = smem_desc(sbase + S::k_off + k * 256, 128, 2048);
+                mma_bf16(tmem, da, db, idesc_qk, k > 0);
+            }
+            mma_commit(&bar_s);
+        }
+        progress(11 + tile * 10);
+        mbar_wait_bounded(&bar_s, tile & 1);
+        progress(12 + tile * 10);
+        tc_fence_after();
+        // 3. masked online softmax of this thread's row; P (bf16) -> smem; O rescale
+        float sv[kTN];
+#pragma unroll
+        for (int c = 0; c < kTN / 32; ++c) tmem_ld32(tS + c * 32, sv + c * 32);
+        float tmax = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < kTN; ++j) {
+            const int ui = tile * kTN + j;
+            bool ok = ui < U && my_ok;
+            if (ok) {
+                const int32_t e = uni[ui];
+                const int64_t u = e & 0x7fffffff;
+                ok = u <= my_pos && (u < sink || e < 0 || u >= my_sb);
+            }
+            sv[j] = ok ? sv[j] * scale : -INFINITY;
+            tmax = fmaxf(tmax, sv[j]);
+        }
+        const float new_m = fmaxf(run_m, tmax);
+        const float alpha = (run_m == -INFINITY) ? 0.f : expf(run_m - new_m);
+        float psum = 0.f;
+        unsigned char* ps = smem + S::p_off;
+#pragma unroll
+        for (int c = 0; c < kTN / 8; ++c) {
+            float p[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const float x = sv[c * 8 + u];
+                p[u] = (x == -INFINITY) ? 0.f : expf(x - new_m);
+                psum += p[u];
+            }
+            *reinterpret_cast<uint4*>(ps + kmajor_off(my_i, c * 8)) =
+                make_uint4(pack_bf16(p[0], p[1]), pack_bf16(p[2], p[3]), pack_bf16(p[4], p[5]), pack_bf16(p[6], p[7]));
+        }
+        run_l = run_l * alpha + psum;
+        run_m = new_m;
+        // tcgen05.ld/st are .sync.aligned: the whole warp rescales if any row needs it
+        if (tile > 0 && __any_sync(0xffffffffu, alpha != 1.0f)) {
+            float ov[32];
+#pragma unroll
+            for (int c = 0; c < kHD / 32; ++c) {
+                tmem_ld32(tO + c * 32, ov);
+#pragma unroll
+                for (int u = 0; u < 32; ++u) ov[u] *= alpha;
+                tmem_st32(tO + c * 32, ov);
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
+        fence_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        // 4. O += P V
+        if (t == 0) {
+            tc_fence_after();
+#pragma unroll
+            for (int k = 0; k < kTN / 16; ++k) {
+                const uint64_t da = smem_desc(sbase + S::p_off + k * 256, 128, 2048);
+                const uint64_t db = smem_desc(sbase + S::v_off + k * 4096, 2048, 128);
+                mma_bf16(tmem + 128, da, db, idesc_pv, (tile > 0 || k > 0) ? 1u : 0u);
+            }
+            mma_commit(&bar_o);
+        }
+        progress(13 + tile * 10);
+    }
+    // ---- epilogue: O / l for this thread's row
+    if (n_tiles > 0) {
+        mbar_wait_bounded(&bar_o, (n_tiles - 1) & 1);
+        tc_fence_after();
+    }
+    {
+        const int hh = hp * hpt + my_i / bs;
+        float* orow = a.out + (static_cast<int64_t>(m * hpm + hh) * a.n_rows + row0 + my_r) * kHD;
+        float ov[32];
+#pragma unroll
+        for (int c = 0; c < kHD / 32; ++c) {
+            if (n_tiles > 0) tmem_ld32(tO + c * 32, ov);
+            if (my_ok) {
+                const float inv = run_l > 0.f ? 1.0f / run_l : NAN;
+#pragma unroll
+                for (int u = 0; u < 32; u += 4)
+                    *reinterpret_cast<float4*>(orow + c * 32 + u) =
+                        make_float4(ov[u] * inv, ov[u + 1] * inv, ov[u + 2] * inv, ov[u + 3] * inv);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (w == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+}
+
+}  // namespace
+
+extern "C" int hp_debug_prefill_progress(int* mapped_word) {
+    return hph::check_cuda(cudaMemcpyToSymbol(g_pf_progress, &mapped_word, sizeof(mapped_word)), "hp_debug_prefill_progress");
+}
+
+extern "C" size_t hp_bsa_prefill_smem_bytes(int32_t max_union) {
+    return PrefillSmem::u_off + static_cast<size_t>(max_union) * 4;
+}
+
+extern "C" int hp_bsa_prefill(const hp_bsa_prefill_args* ap, void* stream) {
+    if (!ap) return hph::set_error(HP_INVALID_ARGUMENT, "hp_bsa_prefill: null args");
+    const hp_bsa_prefill_args& a = *ap;
+    if (a.kv.d != kHD || a.kv.dtype != HP_BF16)
+        return hph::set_error(HP_INVALID_ARGUMENT, "hp_bsa_prefill: the tensor-core path needs bf16 K/V with head_dim 128");
+    if (a.block_size <= 0 || kTM % a.block_size || a.heads_per_mask % (kTM / a.block_size) ||
+        a.n_q_heads % a.heads_per_mask || a.n_q_heads % a.kv.n_kv || (a.n_q_heads / a.kv.n_kv) % a.heads_per_mask)
+        return hph::set_error(HP_INVALID_ARGUMENT,
+                              "hp_bsa_prefill: block_size must divide 128 and 128/block_size heads must share a kv head");
+    if (!a.q || !a.out || !a.mask_list || !a.mask_count || !a.kv.k_pool || !a.kv.v_pool)
+        return hph::set_error(HP_INVALID_ARGUMENT, "hp_bsa_prefill: null pointer");
+    const int n_blocks = (a.n_rows + a.block_size - 1) / a.block_size;
+    if (a.n_mask_blocks < n_blocks) return hph::set_error(HP_INVALID_ARGUMENT, "block_sparse_attention: mask does not cover the queries");
+    const int max_union = a.sink_tokens + a.max_mask + a.stream_tokens + a.block_size;
+    const size_t smem = hp_bsa_prefill_smem_bytes(max_union);
+    if (smem > 227 * 1024) return hph::set_error(HP_INVALID_ARGUMENT, "hp_bsa_prefill: selected set too large (%d keys)", max_union);
+    cudaError_t e = cudaFuncSetAttribute(bsa_prefill_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return hph::check_cuda(e, "bsa_prefill_tc_kernel");
+    const int n_masks = a.n_q_heads / a.heads_per_mask;
+    dim3 grid(n_blocks, n_masks, a.heads_per_mask / (kTM / a.block_size));
+    bsa_prefill_tc_kernel<<<grid, kThreads, smem, static_cast<cudaStream_t>(stream)>>>(a, max_union);
+    return hph::check_cuda(cudaGetLastError(), "bsa_prefill_tc_kernel");
+}

@@ -688,3 +688,21 @@ class CachedKV(PagedKV):
 
     def resident_pages(self) -> int:
         return int((self.page_table >= 0).sum())
+
+
+# ------------------------------------------------------- prefill BSA on tcgen05
+def bsa_prefill_tc(q: torch.Tensor, kv: PagedKV, mask_list: torch.Tensor, mask_count: torch.Tensor, *,
+                   block_size: int, query_offset: int, sink: int, stream_tokens: int,
+                   out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """block_sparse_attention (sparse_attention.cpp:114-145) for a prefill on the tensor
+    cores (hp_bsa_prefill): q fp32 [n_q_heads, T_q, 128]; mask lists [n_masks, n_blocks,
+    stride] (+ counts) as build_mask returns them; bf16 K/V. Returns [n_q_heads, T_q, 128]."""
+    hq, t_q, d = q.shape
+    n_masks, nb, stride = mask_list.shape
+    out = out if out is not None else torch.empty_like(q)
+    a = _capi.BsaPrefillArgs(n_q_heads=hq, heads_per_mask=hq // n_masks, n_rows=t_q, block_size=block_size,
+                             q=_ptr(q), query_offset=query_offset, mask_list=_ptr(mask_list),
+                             mask_count=_ptr(mask_count), mask_stride=stride, n_mask_blocks=nb, max_mask=stride,
+                             sink_tokens=sink, stream_tokens=stream_tokens, out=_ptr(out), kv=kv.view())
+    check(lib().hp_bsa_prefill(C.byref(a), C.c_void_p(_stream(stream))))
+    return out
