@@ -32,7 +32,7 @@ namespace {
 constexpr int kTM = 128;       // query rows per MMA tile (TMEM lanes)
 constexpr int kTN = 128;       // keys per tile
 constexpr int kHD = 128;       // head dim
-constexpr int kThreads = 128;  // one thread per query row
+constexpr int kThreads = 256;  // two threads per query row (64 score columns each)
 constexpr uint32_t kTmemCols = 256;  // S [0,128) + O [128,256)
 
 // canonical no-swizzle layouts, byte offsets (8 x 16 B core matrices)
@@ -134,11 +134,12 @@ __device__ __forceinline__ void progress(int code) {
 }
 
 struct PrefillSmem {
+    static constexpr uint32_t tile_bytes = kTN * kHD * 2;  // 32 KB
     static constexpr uint32_t q_off = 0;
-    static constexpr uint32_t k_off = q_off + kTM * kHD * 2;
-    static constexpr uint32_t v_off = k_off + kTN * kHD * 2;
-    static constexpr uint32_t p_off = v_off + kTN * kHD * 2;
-    static constexpr uint32_t u_off = p_off + kTM * kTN * 2;  // union list (int32, bit 31 = in mask)
+    static constexpr uint32_t k_off = q_off + kTM * kHD * 2;  // K[2] (double buffered)
+    static constexpr uint32_t v_off = k_off + 2 * tile_bytes;  // V[2]
+    static constexpr uint32_t p_off = v_off + 2 * tile_bytes;
+    static constexpr uint32_t u_off = p_off + kTM * kTN * 2;   // union list (int32, bit 31 = in mask)
 };
 
 __global__ void __launch_bounds__(kThreads, 1) bsa_prefill_tc_kernel(const hp_bsa_prefill_args a, int max_union) {
@@ -218,13 +219,14 @@ __global__ void __launch_bounds__(kThreads, 1) bsa_prefill_tc_kernel(const hp_bs
         if (u >= st0 && u <= pos_last) uni[s0 + nmid + (u - st0)] |= static_cast<int32_t>(0x80000000u);
     }
     // ---- Q tile (bf16, K-major): tile row i = head (i / bs) of the pair, block row (i % bs)
+    const int my_i = t & (kTM - 1), half = t >> 7;  // row, score-column half
     {
-        const int i = t;
+        const int i = my_i;
         const int hh = hp * hpt + i / bs, r = i % bs;
         const bool ok = r < rows_here;
         const float* qr = a.q + (static_cast<int64_t>(m * hpm + hh) * a.n_rows + row0 + r) * kHD;
         unsigned char* qs = smem + S::q_off;
-        for (int c = 0; c < kHD / 8; ++c) {
+        for (int c = half * 8; c < half * 8 + 8; ++c) {
             uint4 pk = make_uint4(0, 0, 0, 0);
             if (ok) {
                 const float4 x0 = reinterpret_cast<const float4*>(qr)[2 * c];
@@ -234,92 +236,96 @@ __global__ void __launch_bounds__(kThreads, 1) bsa_prefill_tc_kernel(const hp_bs
             *reinterpret_cast<uint4*>(qs + kmajor_off(i, c * 8)) = pk;
         }
     }
-    const int my_i = t;
     const int my_r = my_i % bs;
     const bool my_ok = my_r < rows_here;
     const int64_t my_pos = pos_first + (my_ok ? my_r : rows_here - 1);
     const int64_t my_sb = stream_begin(my_pos);
     const float scale = 1.0f / sqrtf(static_cast<float>(kHD));
-    float run_m = -INFINITY, run_l = 0.f;
-    const uint32_t lane_base = static_cast<uint32_t>(w * 32) << 16;
-    const uint32_t tS = tmem + lane_base;          // S columns [0, 128)
-    const uint32_t tO = tmem + lane_base + 128;    // O columns [128, 256)
+    float run_m = -INFINITY, run_l = 0.f;  // run_l: this thread's half of the row sum
+    const uint32_t lane_base = static_cast<uint32_t>((w & 3) * 32) << 16;
+    const uint32_t tS = tmem + lane_base + half * 64;        // this half's S columns
+    const uint32_t tO = tmem + lane_base + 128 + half * 64;  // this half's O columns
     const uint32_t idesc_qk = instr_desc(kTM, kTN, 0, 0);
     const uint32_t idesc_pv = instr_desc(kTM, kHD, 0, 1);
     const uint32_t sbase = smem_u32(smem);
     const int n_tiles = (U + kTN - 1) / kTN;
-    for (int tile = 0; tile < n_tiles; ++tile) {
-        // 0. the previous P.V has finished reading P, V (and K via program order)
-        if (tile > 0) {
-            mbar_wait_bounded(&bar_o, (tile - 1) & 1);
-            tc_fence_after();
-        }
-        // 1. gather this tile's K and V rows (thread = key)
-        {
-            const int j = t;
+    __shared__ float sh_max[2][kTM];
+    // coalesced gather: 16 threads per 256 B row (one 16 B chunk each), 16 rows per pass
+    auto gather = [&](int tile, int buf) {
+        unsigned char* ks = smem + S::k_off + buf * S::tile_bytes;
+        unsigned char* vs = smem + S::v_off + buf * S::tile_bytes;
+        const int c = t & 15;
+#pragma unroll 2
+        for (int j0 = 0; j0 < kTN; j0 += kThreads / 16) {
+            const int j = j0 + (t >> 4);
             const int ui = tile * kTN + j;
-            unsigned char* ks = smem + S::k_off;
-            unsigned char* vs = smem + S::v_off;
             if (ui < U) {
                 const int64_t tok = uni[ui] & 0x7fffffff;
                 const char* kp = kv_row_ptr(a.kv, a.kv.k_pool, a.kv.k_host, kvh, tok, 2);
                 const char* vp = kv_row_ptr(a.kv, a.kv.v_pool, a.kv.v_host, kvh, tok, 2);
-#pragma unroll
-                for (int c = 0; c < kHD / 8; ++c) {
-                    cp_async16(ks + kmajor_off(j, c * 8), kp + c * 16);
-                    cp_async16(vs + mnmajor_off(j, c * 8), vp + c * 16);
-                }
+                cp_async16(ks + kmajor_off(j, c * 8), kp + c * 16);
+                cp_async16(vs + mnmajor_off(j, c * 8), vp + c * 16);
             } else {
-#pragma unroll
-                for (int c = 0; c < kHD / 8; ++c) {
-                    *reinterpret_cast<uint4*>(ks + kmajor_off(j, c * 8)) = make_uint4(0, 0, 0, 0);
-                    *reinterpret_cast<uint4*>(vs + mnmajor_off(j, c * 8)) = make_uint4(0, 0, 0, 0);
-                }
+                *reinterpret_cast<uint4*>(ks + kmajor_off(j, c * 8)) = make_uint4(0, 0, 0, 0);
+                *reinterpret_cast<uint4*>(vs + mnmajor_off(j, c * 8)) = make_uint4(0, 0, 0, 0);
             }
         }
+    };
+    if (n_tiles > 0) gather(0, 0);
+    for (int tile = 0; tile < n_tiles; ++tile) {
+        const int buf = tile & 1;
+        // 1. this tile's K/V have landed
         cp_async_wait_all();
         fence_async_smem();
         tc_fence_before();
         __syncthreads();
         progress(10 + tile * 10);
-        // 2. S = Q K^T
+        // 2. S = Q K^T (queued behind the previous P.V on the tensor core)
         if (t == 0) {
             tc_fence_after();
 #pragma unroll
             for (int k = 0; k < kHD / 16; ++k) {
                 const uint64_t da = smem_desc(sbase + S::q_off + k * 256, 128, 2048);
-                const uint64_t db = smem_desc(sbase + S::k_off + k * 256, 128, 2048);
+                const uint64_t db = smem_desc(sbase + S::k_off + buf * S::tile_bytes + k * 256, 128, 2048);
                 mma_bf16(tmem, da, db, idesc_qk, k > 0);
             }
             mma_commit(&bar_s);
         }
+        // 3. the previous P.V is done: its P, V buffer and O are free -> prefetch the next tile
+        if (tile > 0) {
+            mbar_wait_bounded(&bar_o, (tile - 1) & 1);
+            tc_fence_after();
+        }
+        if (tile + 1 < n_tiles) gather(tile + 1, buf ^ 1);
         progress(11 + tile * 10);
         mbar_wait_bounded(&bar_s, tile & 1);
         progress(12 + tile * 10);
         tc_fence_after();
-        // 3. masked online softmax of this thread's row; P (bf16) -> smem; O rescale
-        float sv[kTN];
+        // 4. masked online softmax over this thread's 64 columns; row max shared by the two halves
+        float sv[kTN / 2];
 #pragma unroll
-        for (int c = 0; c < kTN / 32; ++c) tmem_ld32(tS + c * 32, sv + c * 32);
+        for (int c = 0; c < kTN / 64; ++c) tmem_ld32(tS + c * 32, sv + c * 32);
         float tmax = -INFINITY;
 #pragma unroll
-        for (int j = 0; j < kTN; ++j) {
-            const int ui = tile * kTN + j;
+        for (int jj = 0; jj < kTN / 2; ++jj) {
+            const int ui = tile * kTN + half * 64 + jj;
             bool ok = ui < U && my_ok;
             if (ok) {
                 const int32_t e = uni[ui];
                 const int64_t u = e & 0x7fffffff;
                 ok = u <= my_pos && (u < sink || e < 0 || u >= my_sb);
             }
-            sv[j] = ok ? sv[j] * scale : -INFINITY;
-            tmax = fmaxf(tmax, sv[j]);
+            sv[jj] = ok ? sv[jj] * scale : -INFINITY;
+            tmax = fmaxf(tmax, sv[jj]);
         }
-        const float new_m = fmaxf(run_m, tmax);
+        sh_max[half][my_i] = tmax;
+        __syncthreads();
+        const float new_m = fmaxf(run_m, fmaxf(sh_max[0][my_i], sh_max[1][my_i]));
         const float alpha = (run_m == -INFINITY) ? 0.f : expf(run_m - new_m);
         float psum = 0.f;
         unsigned char* ps = smem + S::p_off;
 #pragma unroll
-        for (int c = 0; c < kTN / 8; ++c) {
+        for (int c = 0; c < kTN / 16; ++c) {
             float p[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
@@ -327,7 +333,7 @@ __global__ void __launch_bounds__(kThreads, 1) bsa_prefill_tc_kernel(const hp_bs
                 p[u] = (x == -INFINITY) ? 0.f : expf(x - new_m);
                 psum += p[u];
             }
-            *reinterpret_cast<uint4*>(ps + kmajor_off(my_i, c * 8)) =
+            *reinterpret_cast<uint4*>(ps + kmajor_off(my_i, half * 64 + c * 8)) =
                 make_uint4(pack_bf16(p[0], p[1]), pack_bf16(p[2], p[3]), pack_bf16(p[4], p[5]), pack_bf16(p[6], p[7]));
         }
         run_l = run_l * alpha + psum;
@@ -336,7 +342,7 @@ __global__ void __launch_bounds__(kThreads, 1) bsa_prefill_tc_kernel(const hp_bs
         if (tile > 0 && __any_sync(0xffffffffu, alpha != 1.0f)) {
             float ov[32];
 #pragma unroll
-            for (int c = 0; c < kHD / 32; ++c) {
+            for (int c = 0; c < kHD / 64; ++c) {
                 tmem_ld32(tO + c * 32, ov);
 #pragma unroll
                 for (int u = 0; u < 32; ++u) ov[u] *= alpha;
@@ -347,33 +353,36 @@ __global__ void __launch_bounds__(kThreads, 1) bsa_prefill_tc_kernel(const hp_bs
         fence_async_smem();
         tc_fence_before();
         __syncthreads();
-        // 4. O += P V
+        // 5. O += P V
         if (t == 0) {
             tc_fence_after();
 #pragma unroll
             for (int k = 0; k < kTN / 16; ++k) {
                 const uint64_t da = smem_desc(sbase + S::p_off + k * 256, 128, 2048);
-                const uint64_t db = smem_desc(sbase + S::v_off + k * 4096, 2048, 128);
+                const uint64_t db = smem_desc(sbase + S::v_off + buf * S::tile_bytes + k * 4096, 2048, 128);
                 mma_bf16(tmem + 128, da, db, idesc_pv, (tile > 0 || k > 0) ? 1u : 0u);
             }
             mma_commit(&bar_o);
         }
         progress(13 + tile * 10);
     }
-    // ---- epilogue: O / l for this thread's row
+    // ---- epilogue: O / l for this thread's row and column half
     if (n_tiles > 0) {
         mbar_wait_bounded(&bar_o, (n_tiles - 1) & 1);
         tc_fence_after();
     }
+    sh_max[half][my_i] = run_l;
+    __syncthreads();
+    const float row_l = sh_max[0][my_i] + sh_max[1][my_i];
     {
         const int hh = hp * hpt + my_i / bs;
-        float* orow = a.out + (static_cast<int64_t>(m * hpm + hh) * a.n_rows + row0 + my_r) * kHD;
+        float* orow = a.out + (static_cast<int64_t>(m * hpm + hh) * a.n_rows + row0 + my_r) * kHD + half * 64;
         float ov[32];
 #pragma unroll
-        for (int c = 0; c < kHD / 32; ++c) {
+        for (int c = 0; c < kHD / 64; ++c) {
             if (n_tiles > 0) tmem_ld32(tO + c * 32, ov);
             if (my_ok) {
-                const float inv = run_l > 0.f ? 1.0f / run_l : NAN;
+                const float inv = row_l > 0.f ? 1.0f / row_l : NAN;
 #pragma unroll
                 for (int u = 0; u < 32; u += 4)
                     *reinterpret_cast<float4*>(orow + c * 32 + u) =
