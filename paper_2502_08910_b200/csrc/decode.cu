@@ -731,6 +731,7 @@ __device__ __forceinline__ float warp_sum(float v) {
 // The output matches attention_row within the stated fp32 tolerance (only the
 // summation order differs from the reference's ascending loop).
 constexpr int kBsaThreads = 256;
+constexpr int kBsaRec = kD + 4;  // partial record per (split, head): m, l, pad, pad, o[kD] (16 B aligned)
 constexpr int kBsaMaxKeys = 128;
 constexpr int kBsaMinKeys = 32;
 
@@ -746,8 +747,6 @@ struct BsaSmem {
     static constexpr size_t ml_off = r_off + 4 * HC * kD * 4;
     static constexpr size_t ptr_off = ml_off + ((2 * HC * 4 + 15) / 16) * 16;
     static constexpr size_t bytes = ptr_off + 2 * kBsaMaxKeys * 8;
-    // merge scratch reuses the K rows: (m, l) pairs of every split
-    static constexpr int max_merge_pairs = static_cast<int>((v_off - k_off) / 8);
 };
 
 template <typename T, int HC, bool EXT>
@@ -959,25 +958,36 @@ decode_bsa_kernel(const hp_decode_bsa_args a, float* part, int* tickets, int spl
     __syncthreads();
     trace(2, 4);
     if (cut == 3) return;
-    float* pbase = part + static_cast<int64_t>(hg) * splits * HC * (kD + 2);
+    float* pbase = part + static_cast<int64_t>(hg) * splits * HC * kBsaRec;
     for (int idx = t; idx < HC * kD; idx += kBsaThreads) {
         const int hh = idx / kD, e = idx - hh * kD;
         const float o = red[(0 * HC + hh) * kD + e] + red[(1 * HC + hh) * kD + e] +
                         red[(2 * HC + hh) * kD + e] + red[(3 * HC + hh) * kD + e];
-        float* pp = pbase + (static_cast<int64_t>(split) * HC + hh) * (kD + 2);
+        float* pp = pbase + (static_cast<int64_t>(split) * HC + hh) * kBsaRec;
         if (e == 0) { pp[0] = ml[2 * hh]; pp[1] = ml[2 * hh + 1]; }
-        pp[2 + e] = o;
+        pp[4 + e] = o;
     }
     if (cut == 4) return;
     const bool last_cta = cta_ticket_last(&tickets[hg], splits, &sh_last);
     trace(2, 6);
     if (!last_cta) return;
-    // ---- 4. merge every split of this head group (log-sum-exp)
-    float* mlp = reinterpret_cast<float*>(Ks);  // [splits][HC][2]
-    for (int i = t; i < splits * HC; i += kBsaThreads) {
-        const float* pp = pbase + static_cast<int64_t>(i) * (kD + 2);
-        mlp[2 * i] = __ldcg(pp);
-        mlp[2 * i + 1] = __ldcg(pp + 1);
+    // ---- 4. merge every split of this head group (log-sum-exp). One L2 round trip:
+    //         the first records land in the K/V shared memory by cp.async while every
+    //         split's (m, l) is read into the PV scratch.
+    float* mlp = red;  // [splits][HC][2] (m, l) -> (weight, l); splits <= 2 * kD (host check)
+    constexpr int kStaged = static_cast<int>(S::q_off / (HC * kBsaRec * 4));
+    const int sb = min(splits, kStaged);
+    {
+        const char* src = reinterpret_cast<const char*>(pbase);
+        const int n16 = sb * HC * kBsaRec / 4;
+        for (int i = t; i < n16; i += kBsaThreads) cp_async16(smem + i * 16, src + i * 16);
+        cp_async_commit();
+        for (int i = t; i < splits * HC; i += kBsaThreads) {
+            const float* pp = pbase + static_cast<int64_t>(i) * kBsaRec;
+            mlp[2 * i] = __ldcg(pp);
+            mlp[2 * i + 1] = __ldcg(pp + 1);
+        }
+        cp_async_wait_all();
     }
     __syncthreads();
     {  // head reductions on every warp (warps >= HC discard theirs), no warp-index branch
@@ -1006,24 +1016,13 @@ decode_bsa_kernel(const hp_decode_bsa_args a, float* part, int* tickets, int spl
     }
     __syncthreads();
     trace(2, 5);
+    const float* staged = reinterpret_cast<const float*>(smem);
     for (int idx = t; idx < HC * kD; idx += kBsaThreads) {
         const int hh = idx / kD, e = idx - hh * kD;
-        const float* pb = pbase + static_cast<int64_t>(hh) * (kD + 2) + 2 + e;
         float o = 0.f;
-        constexpr int kBatch = 16;  // independent loads in flight per thread
-        for (int s0 = 0; s0 < splits; s0 += kBatch) {
-            float vals[kBatch];
-#pragma unroll
-            for (int k = 0; k < kBatch; ++k) {
-                const int s = min(s0 + k, splits - 1);
-                vals[k] = __ldcg(pb + static_cast<int64_t>(s) * HC * (kD + 2));
-            }
-#pragma unroll
-            for (int k = 0; k < kBatch; ++k) {
-                const int s = s0 + k;
-                if (s < splits) o = fmaf(vals[k], mlp[2 * (s * HC + hh)], o);
-            }
-        }
+        for (int s = 0; s < sb; ++s) o = fmaf(staged[(s * HC + hh) * kBsaRec + 4 + e], mlp[2 * (s * HC + hh)], o);
+        for (int s = sb; s < splits; ++s)  // records beyond the staging room (large selections)
+            o = fmaf(__ldcg(pbase + static_cast<int64_t>(s * HC + hh) * kBsaRec + 4 + e), mlp[2 * (s * HC + hh)], o);
         const float M = ml[2 * hh], L = ml[2 * hh + 1];
         const int64_t h = h0 + hh;
         a.out[h * kD + e] = L > 0.f ? o / L : NAN;
@@ -1122,7 +1121,7 @@ cudaError_t launch_stage(const hp_decode_stage_args& a, float* scores, int* tick
 template <typename T, int HC, bool EXT>
 cudaError_t launch_bsa(const hp_decode_bsa_args& a, float* part, int* tickets, int splits, int kpc, cudaStream_t s) {
     using S = BsaSmem<T, HC>;
-    if (splits * HC > S::max_merge_pairs) return cudaErrorInvalidValue;
+    if (splits > 2 * kD) return cudaErrorInvalidValue;  // (m, l) of every split fit the PV scratch
     auto kern = decode_bsa_kernel<T, HC, EXT>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(S::bytes));
     if (e != cudaSuccess) return e;
@@ -1243,7 +1242,7 @@ extern "C" int hp_select_topk(const float* scores, int64_t stride, int32_t n_mas
 
 extern "C" size_t hp_decode_bsa_workspace_bytes(int32_t n_q_heads, int32_t max_sel) {
     const int splits = std::max(1, (max_sel + kBsaMinKeys - 1) / kBsaMinKeys);  // bound for any keys/CTA
-    return align_up(static_cast<size_t>(n_q_heads) * splits * (kD + 2) * 4, 256) + align_up(static_cast<size_t>(n_q_heads) * 4, 256);
+    return align_up(static_cast<size_t>(n_q_heads) * splits * kBsaRec * 4, 256) + align_up(static_cast<size_t>(n_q_heads) * 4, 256);
 }
 
 extern "C" int hp_decode_bsa(const hp_decode_bsa_args* ap, void* stream) {

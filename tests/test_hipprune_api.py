@@ -225,3 +225,44 @@ def test_decode_engine_matches_reference_engine(engine_gold, ext):
                     f"step {i} layer {layer} stage {st}"
         assert rel_err(out, g[f"e{ext}_s{i}_out"]) <= RTOL, f"step {i}"
     assert e.steps_taken == 12 and list(e.counters) == [0, 0]
+
+
+def _truncate(full, t_kv, q_len):
+    """truncate_workload (workload.cpp): keys/values [0, t_kv), the last q_len query rows."""
+    L, H = full.num_layers, full.num_heads
+    q = np.stack([np.stack([full.q(l, h)[t_kv - q_len:t_kv] for h in range(H)]) for l in range(L)])
+    k = np.stack([np.stack([full.k(l, h)[:t_kv] for h in range(H)]) for l in range(L)])
+    v = np.stack([np.stack([full.v(l, h)[:t_kv] for h in range(H)]) for l in range(L)])
+    return hp.Workload(np.ascontiguousarray(q), np.ascontiguousarray(k), np.ascontiguousarray(v))
+
+
+@pytest.mark.gpu
+def test_cache_disabled_equivalence_acceptance7():
+    """acceptance.cpp:269-316: with every stage refreshed each step, the engine's last
+    stage cache equals build_mask on the truncated workload and its outputs equal the
+    block-sparse attention of that mask, for 64 steps; then refresh counts over 48 steps
+    at intervals (16, 8, 4) are (3, 6, 12)."""
+    steps = 64
+    full = hp.generate(heads=2, layers=2, seq_kv=144, seq_q=144, dim=8, seed=8001)
+    stages = [(1, 4, 32), (1, 4, 16), (1, 2, 8)]
+    e = hp.DecodeEngine(full, prefill_len=144 - steps, q_len=1, stages=stages, sink=8, stream=16,
+                        refresh=[1, 1, 1], extension=False, page_size=8)
+    e.prefill()
+    for t in range(144 - steps, 144):
+        out, tel = e.step()
+        trunc = _truncate(full, t + 1, 1)
+        for layer in range(2):
+            mask = hp.build_mask(trunc, layer, stages=stages, sink=8, stream=16, extension=False)
+            assert e.stage_cache(layer, 2) == list(mask.indices[0]), (t, layer)
+            want = np.stack(hp.block_sparse_attention(trunc, layer, mask))[:, 0]
+            assert rel_err(out[layer], want) <= RTOL, (t, layer)
+    long_full = hp.generate(heads=1, layers=1, seq_kv=240, seq_q=240, dim=8, seed=8002)
+    counted = hp.DecodeEngine(long_full, prefill_len=192, q_len=1, stages=stages, sink=8, stream=16,
+                              refresh=[16, 8, 4], extension=False, page_size=8)
+    counted.prefill()
+    refreshes = [0, 0, 0]
+    for _ in range(48):
+        _, tel = counted.step()
+        for i in range(3):
+            refreshes[i] += bool(tel["refreshed"][i])
+    assert refreshes == [3, 6, 12]
