@@ -11,7 +11,7 @@ import os
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "_lib" / ("libhipprune_b200_trace.so" if os.environ.get("HP_TRACE") == "1"
+LIB_PATH = PKG / "_lib" / ("libhipprune_b200_trace.so" if os.environ.get("HP_TRACE") in ("1", "cuts")
                            else "libhipprune_b200.so")
 
 HP_OK = 0

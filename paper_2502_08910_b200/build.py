@@ -37,7 +37,9 @@ def _stale(target: Path, deps) -> bool:
 
 def build_cuda(force: bool = False, verbose: bool = False) -> Path:
     LIB.mkdir(exist_ok=True)
-    traced = os.environ.get("HP_TRACE") == "1"  # dev build with the per-CTA phase tracer
+    # dev builds: HP_TRACE=1 -> phase cuts + per-CTA phase tracer; HP_TRACE=cuts -> cuts only
+    traced = os.environ.get("HP_TRACE") in ("1", "cuts")
+    dev_flags = (["-DHP_TRACE"] + (["-DHP_CUTS_ONLY"] if os.environ.get("HP_TRACE") == "cuts" else [])) if traced else []
     out = LIB / ("libhipprune_b200_trace.so" if traced else "libhipprune_b200.so")
     deps = [CSRC / s for s in CUDA_SOURCES] + list(CSRC.glob("*.cuh")) + [ROOT / "include" / "hipprune_b200.h", Path(__file__)]
     if not force and not _stale(out, deps):
@@ -45,7 +47,7 @@ def build_cuda(force: bool = False, verbose: bool = False) -> Path:
     objs, procs = [], []
     for src in CUDA_SOURCES:  # compile translation units in parallel
         obj = LIB / (Path(src).stem + (".trace.o" if traced else ".o"))
-        cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *(["-DHP_TRACE"] if traced else []), "-c", str(CSRC / src), "-o", str(obj)]
+        cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *dev_flags, "-c", str(CSRC / src), "-o", str(obj)]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         procs.append((src, subprocess.Popen(cmd)))
@@ -93,7 +95,7 @@ def build_host(force: bool = False) -> Path:
 
 def build(force: bool = False) -> None:
     build_cuda(force=force)
-    if os.environ.get("HP_TRACE") != "1":
+    if os.environ.get("HP_TRACE") not in ("1", "cuts"):
         build_host(force=force)
 
 

@@ -247,7 +247,7 @@ __device__ __forceinline__ int dev_cut_point(int kernel_id) {
 // Compiled in only with -DHP_TRACE (the dev build `HP_TRACE=1 python -m
 // paper_2502_08910_b200.build`): the enable check is a global load per call site.
 __device__ __forceinline__ void trace(int kernel_id, int slot) {
-#ifndef HP_TRACE
+#if !defined(HP_TRACE) || defined(HP_CUTS_ONLY)
     (void)kernel_id;
     (void)slot;
     return;

@@ -691,9 +691,9 @@ decode_topk_kernel(const hp_decode_stage_args a, const float* scores, int head_p
     __syncthreads();
     trace(3, 1);
     if (cut == 1) return;
-    cta_topk_smem(keys, cc, K, ssel, sh);
+    cta_topk_smem(keys, cc, K, ssel, sh, cut);
     trace(3, 2);
-    if (cut == 2) return;
+    if (cut == 2 || cut >= 10) return;
     for (int i = t; i < K; i += nt) sel[i] = ssel[i];
     const int lastc = ssel[K - 1];
     const int n_out = (K - 1) * lc + min(lc, n_in - lastc * lc);
