@@ -35,6 +35,10 @@ constexpr int kD = 128;
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 constexpr int kStageWarps = 4;     // warps per stage CTA
+#ifndef HP_LOOKAHEAD
+#define HP_LOOKAHEAD 1
+#endif
+constexpr bool kLookahead = HP_LOOKAHEAD != 0;  // two-comparison rounds for the classic stage path
 constexpr int kMaxHC = 8;
 
 __device__ __forceinline__ int64_t ref_token(const hp_list_ref& L, int mask, int64_t pos) {
@@ -372,6 +376,214 @@ decode_stage_kernel(const hp_decode_stage_args a, float* scores, int* tickets, i
     }
     trace(10 + lc, 2);
     (void)tickets;
+}
+
+// ------------------------------------------------ lookahead stage kernel (bf16, no RoPE)
+// The classic kernel's descent is one dependent row gather per comparison (6 for
+// l_c = 32). Here every round after the first gathers the step's mid row AND both
+// possible next mids (the direction is unknown until the compare, the candidates are
+// not), then makes two comparisons: l_c = 32 takes 3 rounds (2 + 3 + 3 rows) instead
+// of 6. The three dots run as independent chains over one q read. Same comparisons
+// on the same fp32 values as the classic kernel, so the same representatives.
+constexpr int kLookSlots = 3;
+
+__device__ __forceinline__ void dot3_bf16x(const unsigned char* r0, const unsigned char* r1, const unsigned char* r2,
+                                           int swz, const uint32_t* qb, float& d0, float& d1, float& d2) {
+    const uint4* q4 = reinterpret_cast<const uint4*>(qb);
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f;
+#pragma unroll 2
+    for (int c = 0; c < 16; ++c) {
+        const int o = (c ^ swz) << 4;
+        const uint4 q = q4[c];
+        const uint4 x = *reinterpret_cast<const uint4*>(r0 + o);
+        const uint4 y = *reinterpret_cast<const uint4*>(r1 + o);
+        const uint4 z = *reinterpret_cast<const uint4*>(r2 + o);
+        a0 = fma_bf16(q.x, x.x, a0, false); a1 = fma_bf16(q.x, y.x, a1, false); a2 = fma_bf16(q.x, z.x, a2, false);
+        a0 = fma_bf16(q.x, x.x, a0, true);  a1 = fma_bf16(q.x, y.x, a1, true);  a2 = fma_bf16(q.x, z.x, a2, true);
+        a0 = fma_bf16(q.y, x.y, a0, false); a1 = fma_bf16(q.y, y.y, a1, false); a2 = fma_bf16(q.y, z.y, a2, false);
+        a0 = fma_bf16(q.y, x.y, a0, true);  a1 = fma_bf16(q.y, y.y, a1, true);  a2 = fma_bf16(q.y, z.y, a2, true);
+        a0 = fma_bf16(q.z, x.z, a0, false); a1 = fma_bf16(q.z, y.z, a1, false); a2 = fma_bf16(q.z, z.z, a2, false);
+        a0 = fma_bf16(q.z, x.z, a0, true);  a1 = fma_bf16(q.z, y.z, a1, true);  a2 = fma_bf16(q.z, z.z, a2, true);
+        a0 = fma_bf16(q.w, x.w, a0, false); a1 = fma_bf16(q.w, y.w, a1, false); a2 = fma_bf16(q.w, z.w, a2, false);
+        a0 = fma_bf16(q.w, x.w, a0, true);  a1 = fma_bf16(q.w, y.w, a1, true);  a2 = fma_bf16(q.w, z.w, a2, true);
+    }
+    d0 = a0; d1 = a1; d2 = a2;
+}
+
+// up to three rows per lane (tok < 0 = none) into slots s * 32 + lane; whole warp calls
+__device__ __forceinline__ void stage_rows3(const hp_kv_view& kv, int kvh, int64_t t0, int64_t t1, int64_t t2,
+                                            unsigned char* wstage, int lane) {
+    using G = RowGeom<bf16_t>;
+    constexpr int chunks = G::bytes / 16;
+    constexpr int rows_per_instr = 32 / chunks;
+    const int c = lane % chunks, sub = lane / chunks;
+    const int64_t tk[kLookSlots] = {t0, t1, t2};
+#pragma unroll
+    for (int sl = 0; sl < kLookSlots; ++sl) {
+        const char* p = tk[sl] >= 0 ? kv_row_ptr(kv, kv.k_pool, kv.k_host, kvh, tk[sl], 2) : nullptr;
+        const unsigned long long pu = reinterpret_cast<unsigned long long>(p);
+        unsigned char* base = wstage + static_cast<size_t>(sl) * 32 * G::stride;
+#pragma unroll
+        for (int r = 0; r < 32; r += rows_per_instr) {
+            const int row = r + sub;
+            const unsigned long long pp = __shfl_sync(0xffffffffu, pu, row);
+            if (pp) cp_async16(base + row * G::stride + ((c ^ (row & (chunks - 1))) << 4),
+                               reinterpret_cast<const char*>(pp) + (c << 4));
+        }
+    }
+    cp_async_wait_all();
+    __syncwarp();
+}
+
+__global__ void __launch_bounds__(kStageWarps * 32, 2)
+decode_stage_look_kernel(const hp_decode_stage_args a, float* scores, int cg, int prefetch) {
+    pdl_trigger();
+    pdl_wait();
+    extern __shared__ __align__(128) unsigned char smem[];
+    using T = bf16_t;
+    using G = RowGeom<T>;
+    const int hpm = a.heads_per_mask;
+    const int m = blockIdx.y;
+    const int64_t n_in = a.in_count ? a.in_count[m] : a.in_count_const;
+    const int lc = a.chunk_size;
+    const int64_t cc = (n_in + lc - 1) / lc;
+    const int K = a.keep / lc;
+    const int chunks_per_cta = 32 * cg;
+    const int64_t chunk0 = static_cast<int64_t>(blockIdx.x) * chunks_per_cta;
+    if (a.scores_out == nullptr && (n_in <= a.keep || cc <= K)) {  // identity (pruning.cpp:159-168)
+        if (blockIdx.x == 0 && a.sel_out) {
+            for (int64_t j = threadIdx.x; j < cc; j += blockDim.x) a.sel_out[static_cast<int64_t>(m) * a.sel_stride + j] = static_cast<int32_t>(j);
+            if (threadIdx.x == 0) a.out_count[m] = static_cast<int32_t>(n_in);
+        }
+        return;
+    }
+    if (chunk0 >= cc) return;
+    const int nwarps = blockDim.x >> 5;
+    unsigned char* stage = smem;  // [nwarps][kLookSlots][32][stride]
+    float* qs = reinterpret_cast<float*>(smem + static_cast<size_t>(nwarps) * kLookSlots * 32 * G::stride);
+    uint32_t* qb = reinterpret_cast<uint32_t*>(qs + hpm * kD);
+    float* red = reinterpret_cast<float*>(qb + hpm * (kD / 2));
+    const int lane = threadIdx.x & 31, w = warp_id();
+    bool q_safe = true;
+    for (int i = threadIdx.x; i < hpm * kD; i += blockDim.x) {
+        const float x = a.q[static_cast<int64_t>(m * hpm) * kD + i];
+        qs[i] = x;
+        q_safe &= q_product_safe(x);
+    }
+    const bool use_fma = __syncthreads_and(q_safe) && a.keys_exact != nullptr && *a.keys_exact != 0;
+    for (int i = threadIdx.x; i < hpm * (kD / 2); i += blockDim.x)
+        qb[i] = (__float_as_uint(qs[2 * i]) >> 16) | (__float_as_uint(qs[2 * i + 1]) & 0xffff0000u);
+    __syncthreads();
+
+    unsigned char* wstage = stage + static_cast<size_t>(w) * kLookSlots * 32 * G::stride;
+    const unsigned char* row0 = wstage + lane * G::stride;
+    const unsigned char* row1 = row0 + 32 * G::stride;
+    const unsigned char* row2 = row1 + 32 * G::stride;
+    const int swz = lane & (G::bytes / 16 - 1);
+    const int n_items = hpm * cg;
+    const int per_warp = (n_items + nwarps - 1) / nwarps;
+    for (int k = 0; k < per_warp; ++k) {
+        const int item_raw = w + k * nwarps;
+        const bool item_ok = item_raw < n_items;
+        const int item = item_ok ? item_raw : n_items - 1;
+        const int hh = item % hpm, grp = item / hpm;
+        const int qh = m * hpm + hh;
+        const int kvh = qh / (a.n_q_heads / a.keys.n_kv);
+        const float* qrow = qs + hh * kD;
+        const uint32_t* qbrow = qb + hh * (kD / 2);
+        const int64_t j = chunk0 + grp * 32 + lane;
+        const bool active = j < cc;
+        const int64_t base = j * lc;
+        const int len = active ? static_cast<int>(min64(lc, n_in - base)) : 0;
+        int64_t t_first = 0;
+        bool contiguous = true;
+        if (active) {
+            t_first = ref_token(a.in, m, base);
+            if (len > 1) contiguous = ref_token(a.in, m, base + len - 1) - t_first == len - 1;
+        }
+        auto token = [&](int i) -> int64_t { return contiguous ? t_first + i : ref_token(a.in, m, base + i); };
+        auto dots = [&](float& d0, float& d1, float& d2) {
+            if (use_fma) {
+                dot3_bf16x(row0, row1, row2, swz, qbrow, d0, d1, d2);
+            } else {
+                d0 = dot_row<T>(row0, swz, qrow);
+                d1 = dot_row<T>(row1, swz, qrow);
+                d2 = dot_row<T>(row2, swz, qrow);
+            }
+        };
+        int first = 1, last = len, it = 0, iters = 0;
+        while ((1 << iters) < len) ++iters;
+        float s1 = 0.f;
+        // round 1: row 0 and the first mid (its two successors warmed in L2)
+        const int mid0 = (1 + len + 1) >> 1;
+        const bool step0 = active && iters > 0;
+        __syncwarp();
+        {
+            int64_t pr = -1, pl = -1;
+            if (prefetch && step0 && iters > 1) {
+                if (mid0 < last) pr = token(((mid0 + last + 1) >> 1) - 1);
+                if (first < mid0 - 1) pl = token(((first + mid0) >> 1) - 1);
+            }
+            stage_rows3(a.keys, kvh, active ? token(0) : -1, step0 ? token(mid0 - 1) : -1, -1, wstage, lane);
+            if (pr >= 0) {
+                const char* p = kv_row_ptr(a.keys, a.keys.k_pool, a.keys.k_host, kvh, pr, 2);
+                prefetch_l2(p); prefetch_l2(p + 128);
+            }
+            if (pl >= 0) {
+                const char* p = kv_row_ptr(a.keys, a.keys.k_pool, a.keys.k_host, kvh, pl, 2);
+                prefetch_l2(p); prefetch_l2(p + 128);
+            }
+        }
+        if (active) {
+            float d0, d1, d2;
+            dots(d0, d1, d2);
+            s1 = d0;
+            if (step0) {
+                if (d1 > s1) { first = mid0; s1 = d1; } else { last = mid0 - 1; }
+                ++it;
+            }
+        }
+        // rounds of two comparisons: the mid row and both candidate next mids
+        for (;;) {
+            const bool go = active && it < iters && first < last;
+            if (!__any_sync(0xffffffffu, go)) break;
+            const int mid = (first + last + 1) >> 1;
+            const bool more = it + 1 < iters;
+            const int mid_r = (go && more && mid < last) ? ((mid + last + 1) >> 1) : 0;
+            const int mid_l = (go && more && first < mid - 1) ? ((first + mid) >> 1) : 0;
+            __syncwarp();
+            stage_rows3(a.keys, kvh, go ? token(mid - 1) : -1, mid_r ? token(mid_r - 1) : -1,
+                        mid_l ? token(mid_l - 1) : -1, wstage, lane);
+            if (go) {
+                float dm, dr, dl;
+                dots(dm, dr, dl);
+                float nx;
+                int nmid;
+                if (dm > s1) { first = mid; s1 = dm; nx = dr; nmid = mid_r; } else { last = mid - 1; nx = dl; nmid = mid_l; }
+                ++it;
+                if (it < iters && first < last) {  // nmid == (first + last + 1) >> 1, staged above
+                    if (nx > s1) { first = nmid; s1 = nx; } else { last = nmid - 1; }
+                    ++it;
+                }
+            }
+        }
+        if (item_ok) red[hh * chunks_per_cta + grp * 32 + lane] = s1;
+        __syncwarp();
+    }
+    __syncthreads();
+    for (int c0 = 0; c0 < chunks_per_cta; c0 += blockDim.x) {
+        const int c = c0 + threadIdx.x;
+        const int64_t jj = chunk0 + c;
+        const bool valid = c < chunks_per_cta && jj < cc;
+        float best = -INFINITY;
+        if (valid) {
+            for (int h = 0; h < hpm; ++h) {
+                const float sc = red[h * chunks_per_cta + c];
+                best = (best < sc) ? sc : best;  // std::max (pruning.cpp:182)
+            }
+            (a.scores_out ? a.scores_out : scores)[static_cast<int64_t>(m) * a.max_chunks + jj] = best;
+        }
+    }
 }
 
 // ------------------------------------------------------ one-wave stage kernel (big stages)
@@ -1093,6 +1305,16 @@ cudaError_t launch_stage(const hp_decode_stage_args& a, float* scores, int* tick
         if (e != cudaSuccess) return e;
         e = launch_pdl(k2, dim3((a.max_chunks + per_cta - 1) / per_cta, a.n_masks), dim3(kAllRowsWarps * 32), smem2, s,
                        a, scores);
+    } else if (!EXT && sizeof(T) == 2 && kLookahead) {
+        // latency-bound descents: two comparisons per gather round (decode_stage_look_kernel)
+        const size_t smem4 = static_cast<size_t>(nw) * kLookSlots * 32 * G::stride + static_cast<size_t>(hpm) * kD * 6 +
+                             static_cast<size_t>(hpm) * 32 * cg * 4;
+        auto k4 = decode_stage_look_kernel;
+        e = cudaFuncSetAttribute(k4, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem4));
+        if (e != cudaSuccess) return e;
+        dim3 grid((a.max_chunks + 32 * cg - 1) / (32 * cg), a.n_masks);
+        const int64_t lanes = static_cast<int64_t>(a.n_masks) * a.max_chunks * hpm;
+        e = launch_pdl(k4, grid, dim3(threads), smem4, s, a, scores, cg, lanes <= 65536 ? 1 : 0);
     } else {
         auto kern = decode_stage_kernel<T, EXT>;
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
