@@ -215,6 +215,7 @@ def main():
     patterns = {"full": (True, True, True), "s23": (False, True, True), "s3": (False, False, True),
                 "bsa": (False, False, False)}
     stream = torch.cuda.Stream(device=dev)
+    side = torch.cuda.Stream(device=dev)
     for ly, qq in zip(layers, qss):
         ly.q.copy_(qq[0])
         for _ in range(3):
@@ -229,8 +230,11 @@ def main():
         torch.cuda.current_stream().wait_stream(stream)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=stream):
+            # stage-cache materialization forks to a side branch and joins at the end
+            side.wait_stream(stream)
             for ly in layers:
-                ly.run(t, refresh=list(fl))
+                ly.run(t, refresh=list(fl), mat_stream=side)
+            stream.wait_stream(side)
         graphs[name] = g
     torch.cuda.synchronize()
     cur = torch.cuda.current_stream()

@@ -13,6 +13,8 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 LIB_PATH = PKG / "_lib" / ("libhipprune_b200_trace.so" if os.environ.get("HP_TRACE") in ("1", "cuts")
                            else "libhipprune_b200.so")
+if os.environ.get("HP_LIB"):  # dev: an alternative build of the kernel library (A/B timing)
+    LIB_PATH = Path(os.environ["HP_LIB"])
 
 HP_OK = 0
 HP_F32, HP_BF16 = 0, 1

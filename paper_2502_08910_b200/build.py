@@ -41,12 +41,17 @@ def build_cuda(force: bool = False, verbose: bool = False) -> Path:
     traced = os.environ.get("HP_TRACE") in ("1", "cuts")
     dev_flags = (["-DHP_TRACE"] + (["-DHP_CUTS_ONLY"] if os.environ.get("HP_TRACE") == "cuts" else [])) if traced else []
     out = LIB / ("libhipprune_b200_trace.so" if traced else "libhipprune_b200.so")
+    # dev A/B builds: HP_VARIANT=name HP_VARIANT_FLAGS="-DX=1" -> _lib/libhipprune_b200_<name>.so
+    variant = os.environ.get("HP_VARIANT")
+    if variant:
+        out = LIB / f"libhipprune_b200_{variant}.so"
+        dev_flags = dev_flags + os.environ.get("HP_VARIANT_FLAGS", "").split()
     deps = [CSRC / s for s in CUDA_SOURCES] + list(CSRC.glob("*.cuh")) + [ROOT / "include" / "hipprune_b200.h", Path(__file__)]
     if not force and not _stale(out, deps):
         return out
     objs, procs = [], []
     for src in CUDA_SOURCES:  # compile translation units in parallel
-        obj = LIB / (Path(src).stem + (".trace.o" if traced else ".o"))
+        obj = LIB / (Path(src).stem + (f".{variant}" if variant else "") + (".trace.o" if traced else ".o"))
         cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *dev_flags, "-c", str(CSRC / src), "-o", str(obj)]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")

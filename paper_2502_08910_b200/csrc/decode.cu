@@ -822,7 +822,10 @@ decode_stage_allrows_kernel(const hp_decode_stage_args a, float* scores) {
 // kept chunk ids land in sel_out in ascending order, and the stage's output count
 // (pruning.cpp:194-199: K-1 full chunks plus the last kept chunk's length) in
 // out_count. With list_out the stage's token list is materialised as well.
-constexpr int kTopkThreads2 = 1024;
+#ifndef HP_TOPK_THREADS
+#define HP_TOPK_THREADS 1024
+#endif
+constexpr int kTopkThreads2 = HP_TOPK_THREADS;
 constexpr int kTopkMaxKeys = 16384;
 
 template <int HP>

@@ -477,7 +477,11 @@ class FusedDecodeLayer:
                                   dtype=torch.uint8, device=dev)
         self._keep = []  # ctypes objects alive across async launches
 
-    def run(self, t: int, refresh=None, stream=None, materialize: bool = True) -> torch.Tensor:
+    def run(self, t: int, refresh=None, stream=None, materialize: bool = True,
+            mat_stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+        """One layer step at context length t. ``mat_stream``: materialize the refreshed
+        stage caches on that stream (forked after the BSA; the caller joins it before the
+        caches are next read) so the copy is off the layer's critical path."""
         S = len(self.stages)
         refresh = list(refresh) if refresh is not None else [True] * S
         pos = t - 1
@@ -527,8 +531,14 @@ class FusedDecodeLayer:
                 counts = (C.c_void_p * n)(*[_ptr(self.count[i]) for i in idx])
                 outs = (C.c_void_p * n)(*[_ptr(self.cache[i]) for i in idx])
                 strides = (C.c_int64 * n)(*[self.cache[i].shape[-1] for i in idx])
+                msp = sp
+                if mat_stream is not None:
+                    ev = torch.cuda.Event()
+                    ev.record(stream if stream is not None else torch.cuda.current_stream())
+                    mat_stream.wait_event(ev)
+                    msp = C.c_void_p(mat_stream.cuda_stream)
                 check(lib().hp_decode_materialize(refs, counts, outs, strides, n, self.n_masks,
-                                                  max(self.stages[i][2] for i in idx), sp))
+                                                  max(self.stages[i][2] for i in idx), msp))
         return self.out
 
     def run_stage(self, t: int, i: int = 0, stream=None, select: bool = True) -> None:

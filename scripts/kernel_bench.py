@@ -30,6 +30,7 @@ pieces = {
     "s3 descent+topk": lambda: layer.run_stage(t, 2),
     "bsa": lambda: layer.run(t, refresh=[False] * 3, materialize=False),
     "full step": lambda: layer.run(t),
+    "full no-mat": lambda: layer.run(t, materialize=False),
 }
 s = torch.cuda.Stream()
 for name, fn in pieces.items():

@@ -309,6 +309,7 @@ def test_fused_decode_refresh_schedule():
     kw = dict(sink=64, stream_tokens=256, n_q_heads=groups * hpm, n_masks=groups)
     fused = D.FusedDecodeLayer(kvf, stages, **kw)
     generic = D.DecodeLayer(kvg, stages, **kw)
+    side = torch.cuda.Stream()
     counters = [0, 0, 0]
     intervals = [4, 2, 1]
     for s in range(steps):
@@ -321,7 +322,7 @@ def test_fused_decode_refresh_schedule():
         qs = torch.from_numpy(q[:, s]).to(dev)
         fused.q.copy_(qs)
         generic.q.copy_(qs.unsqueeze(1))
-        of = fused.run(t, refresh=flags).clone()
+        of = fused.run(t, refresh=flags, mat_stream=side if s % 2 else None).clone()  # side-branch caches too
         og = generic.run(t, refresh=flags).clone()
         torch.cuda.synchronize()
         for i in range(3):
