@@ -945,35 +945,71 @@ __device__ __forceinline__ float warp_sum(float v) {
 //      (acq_rel ticket) merges all splits by log-sum-exp.
 // The output matches attention_row within the stated fp32 tolerance (only the
 // summation order differs from the reference's ascending loop).
+// thread-block cluster / distributed shared memory (sm_90+)
+__device__ __forceinline__ unsigned cluster_ctarank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ unsigned cluster_nctarank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t dsmem_addr(const void* p, unsigned rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ float ld_dsmem(uint32_t addr) {
+    float v;
+    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+    return v;
+}
+
 constexpr int kBsaThreads = 256;
-constexpr int kBsaRec = kD + 4;  // partial record per (split, head): m, l, pad, pad, o[kD] (16 B aligned)
+constexpr int kBsaRec = kD + 4;
+#ifndef HP_BSA_CLUSTER
+#define HP_BSA_CLUSTER 1
+#endif
+constexpr bool kBsaUseCluster = HP_BSA_CLUSTER != 0;  // partial record per (split, head): m, l, pad, pad, o[kD] (16 B aligned)
 constexpr int kBsaMaxKeys = 128;
 constexpr int kBsaMinKeys = 32;
 
-template <typename T, int HC>
+template <typename T, int HC, int MK = kBsaMaxKeys, int NQ = kBsaThreads / 64>
 struct BsaSmem {
     static constexpr int RB = kD * static_cast<int>(sizeof(T));
     static constexpr int KS = RB + 16;
     static constexpr size_t k_off = 0;
-    static constexpr size_t v_off = k_off + static_cast<size_t>(kBsaMaxKeys) * KS;
-    static constexpr size_t q_off = v_off + static_cast<size_t>(kBsaMaxKeys) * RB;
+    static constexpr size_t v_off = k_off + static_cast<size_t>(MK) * KS;
+    static constexpr size_t q_off = v_off + static_cast<size_t>(MK) * RB;
     static constexpr size_t p_off = q_off + HC * kD * 4;
-    static constexpr size_t r_off = p_off + HC * kBsaMaxKeys * 4;
-    static constexpr size_t ml_off = r_off + 4 * HC * kD * 4;
-    static constexpr size_t ptr_off = ml_off + ((2 * HC * 4 + 15) / 16) * 16;
-    static constexpr size_t bytes = ptr_off + 2 * kBsaMaxKeys * 8;
+    static constexpr size_t r_off = p_off + HC * MK * 4;
+    static constexpr size_t ml_off = r_off + static_cast<size_t>(NQ) * HC * kD * 4;
+    static constexpr size_t w_off = ml_off + ((2 * HC * 4 + 15) / 16) * 16;       // merge weights [HC][32]
+    static constexpr size_t ml2_off = w_off + HC * 32 * 4;                          // merged (M, L) [HC][2]
+    static constexpr size_t ptr_off = ml2_off + ((2 * HC * 4 + 15) / 16) * 16;
+    static constexpr size_t bytes = ptr_off + 2 * static_cast<size_t>(MK) * 8;
 };
 
-template <typename T, int HC, bool EXT>
-__global__ void __launch_bounds__(kBsaThreads, 1)
+// CLU: the splits of a head group are one thread-block cluster (<= 16 CTAs, 512
+// threads, up to 256 keys each) and merge through distributed shared memory — no
+// global partials, no ticket; otherwise the last CTA (ticket) merges from global.
+template <typename T, int HC, bool EXT, int NT = kBsaThreads, int MK = kBsaMaxKeys, bool CLU = false>
+__global__ void __launch_bounds__(NT, 1)
 decode_bsa_kernel(const hp_decode_bsa_args a, float* part, int* tickets, int splits, int kpc) {
     pdl_trigger();
     pdl_wait();
-    using S = BsaSmem<T, HC>;
+    constexpr int NQ = NT / 64;  // PV key groups of 32
+    static_assert(MK / NQ == 32, "PV assumes 32 keys per group");
+    using S = BsaSmem<T, HC, MK, NQ>;
     constexpr int RB = S::RB, KS = S::KS;
     constexpr int half = kD / 2;
     extern __shared__ __align__(128) unsigned char smem[];
-    const int cut = dev_cut_point(2);
+    const int cut = CLU ? -1 : dev_cut_point(2);  // a cut CTA would strand its cluster at the barrier
     if (cut == 0) return;
     unsigned char* Ks = smem + S::k_off;
     unsigned char* Vs = smem + S::v_off;
@@ -981,8 +1017,9 @@ decode_bsa_kernel(const hp_decode_bsa_args a, float* part, int* tickets, int spl
     float* ps = reinterpret_cast<float*>(smem + S::p_off);
     float* red = reinterpret_cast<float*>(smem + S::r_off);
     float* ml = reinterpret_cast<float*>(smem + S::ml_off);
+    float* ml2 = reinterpret_cast<float*>(smem + S::ml2_off);
     unsigned long long* kptr = reinterpret_cast<unsigned long long*>(smem + S::ptr_off);  // row addresses
-    unsigned long long* vptr = kptr + kBsaMaxKeys;
+    unsigned long long* vptr = kptr + MK;
     __shared__ int sh_last;
 
     const int t = threadIdx.x, lane = t & 31, w = warp_id();
@@ -1012,7 +1049,7 @@ decode_bsa_kernel(const hp_decode_bsa_args a, float* part, int* tickets, int spl
         vptr[t] = reinterpret_cast<unsigned long long>(kv_row_ptr(a.kv, a.kv.v_pool, a.kv.v_host, kvh, tok, sizeof(T)));
     }
     if (cut == 5) return;
-    for (int i = t; i < HC * kD; i += kBsaThreads) qs[i] = a.q[static_cast<int64_t>(h0) * kD + i];
+    for (int i = t; i < HC * kD; i += NT) qs[i] = a.q[static_cast<int64_t>(h0) * kD + i];
     __syncthreads();
     if (cut == 6) return;
     {
@@ -1022,14 +1059,14 @@ decode_bsa_kernel(const hp_decode_bsa_args a, float* part, int* tickets, int spl
         constexpr int RPI = 32 / CH;
         const int c = lane % CH, sub = lane / CH;
 #pragma unroll
-        for (int i = 0; i < kBsaMaxKeys / (kBsaThreads / 32) / RPI; ++i) {
-            const int r = (i * (kBsaThreads / 32) + w) * RPI + sub;
+        for (int i = 0; i < MK / (NT / 32) / RPI; ++i) {
+            const int r = (i * (NT / 32) + w) * RPI + sub;
             if (r < nv) cp_async16(Ks + r * KS + c * 16, reinterpret_cast<const char*>(kptr[r]) + c * 16);
         }
         cp_async_commit();
 #pragma unroll
-        for (int i = 0; i < kBsaMaxKeys / (kBsaThreads / 32) / RPI; ++i) {
-            const int r = (i * (kBsaThreads / 32) + w) * RPI + sub;
+        for (int i = 0; i < MK / (NT / 32) / RPI; ++i) {
+            const int r = (i * (NT / 32) + w) * RPI + sub;
             if (r < nv) cp_async16(Vs + r * RB + c * 16, reinterpret_cast<const char*>(vptr[r]) + c * 16);
         }
         cp_async_commit();
@@ -1038,7 +1075,7 @@ decode_bsa_kernel(const hp_decode_bsa_args a, float* part, int* tickets, int spl
         __syncthreads();
         const float* cs = a.rope.cos_tab + pos * half;
         const float* sn = a.rope.sin_tab + pos * half;
-        for (int i = t; i < HC * half; i += kBsaThreads) {
+        for (int i = t; i < HC * half; i += NT) {
             const int hh = i / half, e = i - hh * half;
             float* row = qs + hh * kD;
             const float x = row[e], y = row[e + half], c = cs[e], s = sn[e];
@@ -1054,7 +1091,7 @@ decode_bsa_kernel(const hp_decode_bsa_args a, float* part, int* tickets, int spl
     if (cut == 1) return;
 
     // ---- 2. QK: key j = jb + w*16 + (lane & 15), elements [hf*64, hf*64 + 64)
-    for (int jb = 0; jb < kpc; jb += (kBsaThreads / 32) * 16) {
+    for (int jb = 0; jb < kpc; jb += (NT / 32) * 16) {
         const int j = jb + w * 16 + (lane & 15), hf = lane >> 4;
         float acc[HC];
 #pragma unroll
@@ -1105,9 +1142,9 @@ decode_bsa_kernel(const hp_decode_bsa_args a, float* part, int* tickets, int spl
         }
 #pragma unroll
         for (int hh = 0; hh < HC; ++hh) acc[hh] += __shfl_xor_sync(0xffffffffu, acc[hh], 16);
-        if (hf == 0 && j < kBsaMaxKeys) {
+        if (hf == 0 && j < MK) {
 #pragma unroll
-            for (int hh = 0; hh < HC; ++hh) ps[hh * kBsaMaxKeys + j] = j < nv ? acc[hh] * scale : -INFINITY;
+            for (int hh = 0; hh < HC; ++hh) ps[hh * MK + j] = j < nv ? acc[hh] * scale : -INFINITY;
         }
     }
     __syncthreads();
@@ -1118,15 +1155,15 @@ decode_bsa_kernel(const hp_decode_bsa_args a, float* part, int* tickets, int spl
        // no warp-index branch around the shuffles
         const int hw = w % HC;
         const bool mine = w < HC;
-        float* pr = ps + hw * kBsaMaxKeys;
+        float* pr = ps + hw * MK;
         float mx = -INFINITY;
         for (int j = lane; j < nv; j += 32) mx = fmaxf(mx, pr[j]);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
         float l = 0.f;
-        float pv[kBsaMaxKeys / 32];
+        float pv[MK / 32];
 #pragma unroll
-        for (int i = 0; i < kBsaMaxKeys / 32; ++i) {
+        for (int i = 0; i < MK / 32; ++i) {
             const int j = i * 32 + lane;
             pv[i] = (j < nv && mx != -INFINITY) ? expf(pr[j] - mx) : 0.f;
             l += pv[i];
@@ -1135,7 +1172,7 @@ decode_bsa_kernel(const hp_decode_bsa_args a, float* part, int* tickets, int spl
         __syncthreads();  // every warp has read its scores before the owners overwrite them
         if (mine) {
 #pragma unroll
-            for (int i = 0; i < kBsaMaxKeys / 32; ++i) pr[i * 32 + lane] = pv[i];
+            for (int i = 0; i < MK / 32; ++i) pr[i * 32 + lane] = pv[i];
             if (lane == 0) { ml[2 * w] = mx; ml[2 * w + 1] = l; }
         }
     }
@@ -1147,7 +1184,7 @@ decode_bsa_kernel(const hp_decode_bsa_args a, float* part, int* tickets, int spl
         float o0[HC], o1[HC];
 #pragma unroll
         for (int hh = 0; hh < HC; ++hh) o0[hh] = o1[hh] = 0.f;
-        const int j0 = kq * (kBsaMaxKeys / 4), j1 = min(nv, j0 + kBsaMaxKeys / 4);
+        const int j0 = kq * (MK / NQ), j1 = min(nv, j0 + MK / NQ);
         for (int j = j0; j < j1; ++j) {
             float vx, vy;
             if constexpr (sizeof(T) == 2) {
@@ -1159,7 +1196,7 @@ decode_bsa_kernel(const hp_decode_bsa_args a, float* part, int* tickets, int spl
             }
 #pragma unroll
             for (int hh = 0; hh < HC; ++hh) {
-                const float p = ps[hh * kBsaMaxKeys + j];
+                const float p = ps[hh * MK + j];
                 o0[hh] = fmaf(p, vx, o0[hh]);
                 o1[hh] = fmaf(p, vy, o1[hh]);
             }
@@ -1173,11 +1210,59 @@ decode_bsa_kernel(const hp_decode_bsa_args a, float* part, int* tickets, int spl
     __syncthreads();
     trace(2, 4);
     if (cut == 3) return;
+    if constexpr (CLU) {
+        // ---- 4'. merge across the cluster: this split's (m, l) and summed o stay in its
+        //          shared memory; after one cluster barrier every CTA reads all splits'
+        //          (m, l) and merges its slice of the outputs over DSMEM
+        for (int idx = t; idx < HC * kD; idx += NT) {
+            const int hh = idx / kD, e = idx - hh * kD;
+            float o = red[hh * kD + e];
+#pragma unroll
+            for (int g = 1; g < NQ; ++g) o += red[(g * HC + hh) * kD + e];
+            red[idx] = o;
+        }
+        cluster_sync_all();
+        const unsigned rank = cluster_ctarank(), ncl = cluster_nctarank();
+        float* wts = reinterpret_cast<float*>(smem + S::w_off);  // [HC][32]: weights, then M, L at [HC*32 + 2*hh]
+        {
+            const int hh = w % HC;
+            const bool mine = w < HC;
+            float mo = -INFINITY, lo = 0.f;
+            if (static_cast<unsigned>(lane) < ncl) {
+                const uint32_t r = dsmem_addr(ml, lane);
+                mo = ld_dsmem(r + 8 * hh);
+                lo = ld_dsmem(r + 8 * hh + 4);
+            }
+            float M = lo > 0.f ? mo : -INFINITY;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+            const float f = lo > 0.f ? expf(mo - M) : 0.f;
+            const float L = warp_sum(lo * f);
+            if (mine) wts[hh * 32 + lane] = f;
+            if (mine && lane == 0) { ml2[2 * hh] = M; ml2[2 * hh + 1] = L; }
+        }
+        __syncthreads();
+        const int chunk = (HC * kD + static_cast<int>(ncl) - 1) / static_cast<int>(ncl);
+        const int i0 = static_cast<int>(rank) * chunk, i1 = min(HC * kD, i0 + chunk);
+        for (int idx = i0 + t; idx < i1; idx += NT) {
+            const int hh = idx / kD, e = idx - hh * kD;
+            float o = 0.f;
+            for (unsigned sr = 0; sr < ncl; ++sr) o = fmaf(ld_dsmem(dsmem_addr(red + idx, sr)), wts[hh * 32 + sr], o);
+            const float M = ml2[2 * hh], L = ml2[2 * hh + 1];
+            const int64_t h = h0 + hh;
+            a.out[h * kD + e] = L > 0.f ? o / L : NAN;
+            if (a.part_o) a.part_o[h * kD + e] = L > 0.f ? o / L : 0.f;
+            if (e == 0 && a.part_m) { a.part_m[h] = M; a.part_l[h] = L; }
+        }
+        cluster_sync_all();  // no CTA leaves while its shared memory may still be read
+        return;
+    }
     float* pbase = part + static_cast<int64_t>(hg) * splits * HC * kBsaRec;
-    for (int idx = t; idx < HC * kD; idx += kBsaThreads) {
+    for (int idx = t; idx < HC * kD; idx += NT) {
         const int hh = idx / kD, e = idx - hh * kD;
-        const float o = red[(0 * HC + hh) * kD + e] + red[(1 * HC + hh) * kD + e] +
-                        red[(2 * HC + hh) * kD + e] + red[(3 * HC + hh) * kD + e];
+        float o = red[hh * kD + e];
+#pragma unroll
+        for (int g = 1; g < NQ; ++g) o += red[(g * HC + hh) * kD + e];
         float* pp = pbase + (static_cast<int64_t>(split) * HC + hh) * kBsaRec;
         if (e == 0) { pp[0] = ml[2 * hh]; pp[1] = ml[2 * hh + 1]; }
         pp[4 + e] = o;
@@ -1195,9 +1280,9 @@ decode_bsa_kernel(const hp_decode_bsa_args a, float* part, int* tickets, int spl
     {
         const char* src = reinterpret_cast<const char*>(pbase);
         const int n16 = sb * HC * kBsaRec / 4;
-        for (int i = t; i < n16; i += kBsaThreads) cp_async16(smem + i * 16, src + i * 16);
+        for (int i = t; i < n16; i += NT) cp_async16(smem + i * 16, src + i * 16);
         cp_async_commit();
-        for (int i = t; i < splits * HC; i += kBsaThreads) {
+        for (int i = t; i < splits * HC; i += NT) {
             const float* pp = pbase + static_cast<int64_t>(i) * kBsaRec;
             mlp[2 * i] = __ldcg(pp);
             mlp[2 * i + 1] = __ldcg(pp + 1);
@@ -1232,7 +1317,7 @@ decode_bsa_kernel(const hp_decode_bsa_args a, float* part, int* tickets, int spl
     __syncthreads();
     trace(2, 5);
     const float* staged = reinterpret_cast<const float*>(smem);
-    for (int idx = t; idx < HC * kD; idx += kBsaThreads) {
+    for (int idx = t; idx < HC * kD; idx += NT) {
         const int hh = idx / kD, e = idx - hh * kD;
         float o = 0.f;
         for (int s = 0; s < sb; ++s) o = fmaf(staged[(s * HC + hh) * kBsaRec + 4 + e], mlp[2 * (s * HC + hh)], o);
@@ -1351,6 +1436,45 @@ cudaError_t launch_bsa(const hp_decode_bsa_args& a, float* part, int* tickets, i
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(S::bytes));
     if (e != cudaSuccess) return e;
     e = launch_pdl(kern, dim3(splits, a.n_q_heads / HC), dim3(kBsaThreads), S::bytes, s, a, part, tickets, splits, kpc);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
+// cluster variant: grid (splits, groups), cluster (splits, 1, 1), bf16 without RoPE
+constexpr int kBsaCluThreads = 512, kBsaCluMaxKeys = 256, kBsaMaxCluster = 16;
+template <int HC>
+cudaError_t launch_bsa_cluster(const hp_decode_bsa_args& a, int splits, int kpc, cudaStream_t s) {
+    using S = BsaSmem<bf16_t, HC, kBsaCluMaxKeys, kBsaCluThreads / 64>;
+    auto kern = decode_bsa_kernel<bf16_t, HC, false, kBsaCluThreads, kBsaCluMaxKeys, true>;
+    static int checked_splits[kBsaMaxCluster + 1] = {};  // max active clusters, -1 = none
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(S::bytes));
+    if (e != cudaSuccess) return e;
+    if (splits > 8 && (e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess)
+        return e;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(splits, a.n_q_heads / HC);
+    cfg.blockDim = dim3(kBsaCluThreads);
+    cfg.dynamicSmemBytes = S::bytes;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = splits;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    if (checked_splits[splits] == 0) {  // how many clusters of this size fit at once (GPC-bound)
+        int n = 0;
+        e = cudaOccupancyMaxActiveClusters(&n, kern, &cfg);
+        checked_splits[splits] = (e == cudaSuccess && n > 0) ? n : -1;
+        cudaGetLastError();
+    }
+    // every head group's cluster resident in one wave, else the ticket path is faster
+    // (B200, 162 KB CTAs: 7 clusters of 11-16 fit, 15 of 7-9)
+    if (checked_splits[splits] < static_cast<int>(cfg.gridDim.y)) return cudaErrorNotSupported;
+    e = cudaLaunchKernelEx(&cfg, kern, a, static_cast<float*>(nullptr), static_cast<int*>(nullptr), splits, kpc);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
@@ -1498,6 +1622,21 @@ extern "C" int hp_decode_bsa(const hp_decode_bsa_args* ap, void* stream) {
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const bool ext = a.rope.extension != 0;
     cudaError_t e;
+    if (a.kv.dtype == HP_BF16 && !ext && kBsaUseCluster) {
+        // one cluster per head group when the selection fits 16 CTAs of <= 256 keys
+        const int64_t kc = std::max<int64_t>(kBsaMaxKeys, ((max_sel + kBsaMaxCluster - 1) / kBsaMaxCluster + 15) / 16 * 16);
+        const int sc = static_cast<int>((max_sel + kc - 1) / kc);
+        if (kc <= kBsaCluMaxKeys && sc >= 2 && sc <= kBsaMaxCluster) {
+            switch (hc) {
+                case 1: e = launch_bsa_cluster<1>(a, sc, static_cast<int>(kc), s); break;
+                case 2: e = launch_bsa_cluster<2>(a, sc, static_cast<int>(kc), s); break;
+                case 4: e = launch_bsa_cluster<4>(a, sc, static_cast<int>(kc), s); break;
+                default: e = launch_bsa_cluster<8>(a, sc, static_cast<int>(kc), s); break;
+            }
+            if (e == cudaSuccess) return HP_OK;
+            cudaGetLastError();  // not resident-able here: the ticket path below
+        }
+    }
     if (a.kv.dtype == HP_BF16) e = ext ? dispatch_bsa_hc<bf16_t, true>(a, hc, part, tickets, splits, kpc, s) : dispatch_bsa_hc<bf16_t, false>(a, hc, part, tickets, splits, kpc, s);
     else e = ext ? dispatch_bsa_hc<float, true>(a, hc, part, tickets, splits, kpc, s) : dispatch_bsa_hc<float, false>(a, hc, part, tickets, splits, kpc, s);
     return hph::check_cuda(e, "decode_bsa_kernel");

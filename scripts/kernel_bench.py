@@ -8,7 +8,7 @@ import torch
 from paper_2502_08910_b200 import device as D, synth
 
 t = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 20
-groups, hpm, d = 8, 4, 128
+groups, hpm, d = (int(sys.argv[2]) if len(sys.argv) > 2 else 8), 4, 128
 stages = [(64, 256, 32768), (64, 32, 8192), (64, 8, 2048)]
 q, k, v = synth.generate(groups * hpm, groups, t, d, seed=1)
 kv = D.PagedKV(k, v, page_size=64)
