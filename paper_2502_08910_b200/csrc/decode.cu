@@ -1709,8 +1709,8 @@ extern "C" int hp_decode_materialize(const hp_list_ref* refs, const int32_t* con
         m.stride[i] = out_strides[i];
     }
     const int blocks = std::max(1, std::min(64, (max_count + 255) / 256));
-    const cudaError_t e = launch_pdl(materialize_kernel, dim3(blocks, n_masks, n_lists), dim3(256), 0,
-                                     static_cast<cudaStream_t>(stream), m);
-    if (e != cudaSuccess) return hph::check_cuda(e, "materialize_kernel");
+    // plain launch (no programmatic edge): the caches are usually refreshed on a side
+    // branch of the step graph, off the layer's critical path (FusedDecodeLayer.run)
+    materialize_kernel<<<dim3(blocks, n_masks, n_lists), dim3(256), 0, static_cast<cudaStream_t>(stream)>>>(m);
     return hph::check_cuda(cudaGetLastError(), "materialize_kernel");
 }
