@@ -181,7 +181,7 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
 // same way. Optionally warms L2 with the lane's two possible next-step rows
 // (pf0/pf1, -1 = none): the descent direction is unknown until the compare, but
 // both candidates are (latency-bound stages only). Whole warp must call.
-template <typename T>
+template <typename T, bool WAIT = true>
 __device__ __forceinline__ void stage_rows(const hp_kv_view& kv, int kvh, int64_t tok,
                                            unsigned char* wstage, int lane, int64_t pf0 = -1,
                                            int64_t pf1 = -1) {
@@ -208,8 +208,10 @@ __device__ __forceinline__ void stage_rows(const hp_kv_view& kv, int kvh, int64_
 #pragma unroll
         for (int o = 0; o < G::bytes; o += 128) prefetch_l2(q1 + o);
     }
-    cp_async_wait_all();
-    __syncwarp();
+    if constexpr (WAIT) {
+        cp_async_wait_all();
+        __syncwarp();
+    }
 }
 
 // ------------------------------------------------------------------ stage kernel
@@ -411,6 +413,7 @@ __device__ __forceinline__ void dot3_bf16x(const unsigned char* r0, const unsign
 }
 
 // up to three rows per lane (tok < 0 = none) into slots s * 32 + lane; whole warp calls
+template <bool WAIT = true>
 __device__ __forceinline__ void stage_rows3(const hp_kv_view& kv, int kvh, int64_t t0, int64_t t1, int64_t t2,
                                             unsigned char* wstage, int lane) {
     using G = RowGeom<bf16_t>;
@@ -431,8 +434,10 @@ __device__ __forceinline__ void stage_rows3(const hp_kv_view& kv, int kvh, int64
                                reinterpret_cast<const char*>(pp) + (c << 4));
         }
     }
-    cp_async_wait_all();
-    __syncwarp();
+    if constexpr (WAIT) {
+        cp_async_wait_all();
+        __syncwarp();
+    }
 }
 
 __global__ void __launch_bounds__(kStageWarps * 32, 2)
@@ -460,21 +465,14 @@ decode_stage_look_kernel(const hp_decode_stage_args a, float* scores, int cg, in
     if (chunk0 >= cc) return;
     const int nwarps = blockDim.x >> 5;
     unsigned char* stage = smem;  // [nwarps][kLookSlots][32][stride]
-    float* qs = reinterpret_cast<float*>(smem + static_cast<size_t>(nwarps) * kLookSlots * 32 * G::stride);
-    uint32_t* qb = reinterpret_cast<uint32_t*>(qs + hpm * kD);
-    float* red = reinterpret_cast<float*>(qb + hpm * (kD / 2));
+    // per-warp q of its current head (fp32 + packed bf16 pairs): warp-private, so the
+    // prologue needs no CTA barrier and q staging overlaps the first gather
+    float* qw_all = reinterpret_cast<float*>(smem + static_cast<size_t>(nwarps) * kLookSlots * 32 * G::stride);
+    float* red = qw_all + nwarps * (kD + kD / 2);  // [hpm][chunks_per_cta]
     const int lane = threadIdx.x & 31, w = warp_id();
-    bool q_safe = true;
-    for (int i = threadIdx.x; i < hpm * kD; i += blockDim.x) {
-        const float x = a.q[static_cast<int64_t>(m * hpm) * kD + i];
-        qs[i] = x;
-        q_safe &= q_product_safe(x);
-    }
-    const bool use_fma = __syncthreads_and(q_safe) && a.keys_exact != nullptr && *a.keys_exact != 0;
-    for (int i = threadIdx.x; i < hpm * (kD / 2); i += blockDim.x)
-        qb[i] = (__float_as_uint(qs[2 * i]) >> 16) | (__float_as_uint(qs[2 * i + 1]) & 0xffff0000u);
-    __syncthreads();
-
+    float* qrow = qw_all + w * (kD + kD / 2);
+    uint32_t* qbrow = reinterpret_cast<uint32_t*>(qrow + kD);
+    const bool keys_ok = a.keys_exact != nullptr && *a.keys_exact != 0;
     unsigned char* wstage = stage + static_cast<size_t>(w) * kLookSlots * 32 * G::stride;
     const unsigned char* row0 = wstage + lane * G::stride;
     const unsigned char* row1 = row0 + 32 * G::stride;
@@ -489,8 +487,6 @@ decode_stage_look_kernel(const hp_decode_stage_args a, float* scores, int cg, in
         const int hh = item % hpm, grp = item / hpm;
         const int qh = m * hpm + hh;
         const int kvh = qh / (a.n_q_heads / a.keys.n_kv);
-        const float* qrow = qs + hh * kD;
-        const uint32_t* qbrow = qb + hh * (kD / 2);
         const int64_t j = chunk0 + grp * 32 + lane;
         const bool active = j < cc;
         const int64_t base = j * lc;
@@ -502,6 +498,7 @@ decode_stage_look_kernel(const hp_decode_stage_args a, float* scores, int cg, in
             if (len > 1) contiguous = ref_token(a.in, m, base + len - 1) - t_first == len - 1;
         }
         auto token = [&](int i) -> int64_t { return contiguous ? t_first + i : ref_token(a.in, m, base + i); };
+        bool use_fma = false;
         auto dots = [&](float& d0, float& d1, float& d2) {
             if (use_fma) {
                 dot3_bf16x(row0, row1, row2, swz, qbrow, d0, d1, d2);
@@ -524,7 +521,7 @@ decode_stage_look_kernel(const hp_decode_stage_args a, float* scores, int cg, in
                 if (mid0 < last) pr = token(((mid0 + last + 1) >> 1) - 1);
                 if (first < mid0 - 1) pl = token(((first + mid0) >> 1) - 1);
             }
-            stage_rows3(a.keys, kvh, active ? token(0) : -1, step0 ? token(mid0 - 1) : -1, -1, wstage, lane);
+            stage_rows3<false>(a.keys, kvh, active ? token(0) : -1, step0 ? token(mid0 - 1) : -1, -1, wstage, lane);
             if (pr >= 0) {
                 const char* p = kv_row_ptr(a.keys, a.keys.k_pool, a.keys.k_host, kvh, pr, 2);
                 prefetch_l2(p); prefetch_l2(p + 128);
@@ -533,6 +530,24 @@ decode_stage_look_kernel(const hp_decode_stage_args a, float* scores, int cg, in
                 const char* p = kv_row_ptr(a.keys, a.keys.k_pool, a.keys.k_host, kvh, pl, 2);
                 prefetch_l2(p); prefetch_l2(p + 128);
             }
+        }
+        {  // this head's q while the rows are in flight (the previous item's dots are done: __syncwarp above)
+            bool safe = true;
+#pragma unroll
+            for (int i = 0; i < kD / 32; ++i) {
+                const float x = a.q[static_cast<int64_t>(qh) * kD + i * 32 + lane];
+                qrow[i * 32 + lane] = x;
+                safe &= q_product_safe(x);
+            }
+            use_fma = __all_sync(0xffffffffu, safe) && keys_ok;
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < kD / 64; ++i) {
+                const int e = i * 32 + lane;
+                qbrow[e] = (__float_as_uint(qrow[2 * e]) >> 16) | (__float_as_uint(qrow[2 * e + 1]) & 0xffff0000u);
+            }
+            cp_async_wait_all();
+            __syncwarp();
         }
         if (active) {
             float d0, d1, d2;
@@ -734,6 +749,17 @@ decode_stage_allrows_kernel(const hp_decode_stage_args a, float* scores) {
     unsigned char* wstage = smem + static_cast<size_t>(w) * 32 * G::stride;
     float* qs = reinterpret_cast<float*>(smem + static_cast<size_t>(kAllRowsWarps) * 32 * G::stride);
     uint32_t* qb = reinterpret_cast<uint32_t*>(qs + hpm * kD);
+    // the row gather goes out first; q staging and the exactness check overlap it
+    const int cl = lane / lc, r = lane - cl * lc;  // lane -> (chunk of the warp, row)
+    const int64_t j = (static_cast<int64_t>(blockIdx.x) * kAllRowsWarps + w) * cpw + cl;
+    const bool live = j < cc && cl < cpw;
+    const int kvh = (m * hpm) / (a.n_q_heads / a.keys.n_kv);
+    const int64_t base = j * lc;
+    const int len = live ? static_cast<int>(min64(lc, n_in - base)) : 0;
+    const int64_t tok = r < len ? ref_token(a.in, m, base + r) : -1;
+    if (cut == 2 && tok == 123456789) scores[0] = 0.f;
+    if (cut == 2) return;
+    stage_rows<T, false>(a.keys, kvh, tok, wstage, lane);
     bool q_safe = true;
     for (int i = threadIdx.x; i < hpm * kD; i += blockDim.x) {
         const float x = a.q[static_cast<int64_t>(m * hpm) * kD + i];
@@ -747,16 +773,8 @@ decode_stage_allrows_kernel(const hp_decode_stage_args a, float* scores) {
     }
     __syncthreads();  // unconditional (see decode_stage_kernel)
     if (cut == 1) return;
-    const int cl = lane / lc, r = lane - cl * lc;  // lane -> (chunk of the warp, row)
-    const int64_t j = (static_cast<int64_t>(blockIdx.x) * kAllRowsWarps + w) * cpw + cl;
-    const bool live = j < cc && cl < cpw;
-    const int kvh = (m * hpm) / (a.n_q_heads / a.keys.n_kv);
-    const int64_t base = j * lc;
-    const int len = live ? static_cast<int>(min64(lc, n_in - base)) : 0;
-    const int64_t tok = r < len ? ref_token(a.in, m, base + r) : -1;
-    if (cut == 2 && tok == 123456789) scores[0] = 0.f;
-    if (cut == 2) return;
-    stage_rows<T>(a.keys, kvh, tok, wstage, lane);
+    cp_async_wait_all();
+    __syncwarp();
     if (cut == 3) return;
     const unsigned char* row = wstage + lane * G::stride;
     const int swz = lane & (G::bytes / 16 - 1);
@@ -769,7 +787,27 @@ decode_stage_allrows_kernel(const hp_decode_stage_args a, float* scores) {
 #pragma unroll
         for (int u = 0; u < kAllRowsHeads; ++u) acc[u] = 0.0f;
         const int nh = min(kAllRowsHeads, hpm - h0);
-        if (use_fma) {
+        if (use_fma && nh == kAllRowsHeads) {  // full group of heads: constant q offsets, no index math
+            const uint4* q4 = reinterpret_cast<const uint4*>(qb + h0 * (kD / 2));
+            uint4 wv[16];
+#pragma unroll
+            for (int c = 0; c < 16; ++c) wv[c] = *reinterpret_cast<const uint4*>(row + ((c ^ swz) << 4));
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+#pragma unroll
+                for (int u = 0; u < kAllRowsHeads; ++u) {
+                    const uint4 q = q4[u * 16 + c];  // broadcast
+                    acc[u] = fma_bf16(q.x, wv[c].x, acc[u], false);
+                    acc[u] = fma_bf16(q.x, wv[c].x, acc[u], true);
+                    acc[u] = fma_bf16(q.y, wv[c].y, acc[u], false);
+                    acc[u] = fma_bf16(q.y, wv[c].y, acc[u], true);
+                    acc[u] = fma_bf16(q.z, wv[c].z, acc[u], false);
+                    acc[u] = fma_bf16(q.z, wv[c].z, acc[u], true);
+                    acc[u] = fma_bf16(q.w, wv[c].w, acc[u], false);
+                    acc[u] = fma_bf16(q.w, wv[c].w, acc[u], true);
+                }
+            }
+        } else if (use_fma) {
             const uint4* q4 = reinterpret_cast<const uint4*>(qb + h0 * (kD / 2));
 #pragma unroll 2
             for (int c = 0; c < 16; ++c) {
@@ -1395,7 +1433,7 @@ cudaError_t launch_stage(const hp_decode_stage_args& a, float* scores, int* tick
                        a, scores);
     } else if (!EXT && sizeof(T) == 2 && kLookahead) {
         // latency-bound descents: two comparisons per gather round (decode_stage_look_kernel)
-        const size_t smem4 = static_cast<size_t>(nw) * kLookSlots * 32 * G::stride + static_cast<size_t>(hpm) * kD * 6 +
+        const size_t smem4 = static_cast<size_t>(nw) * kLookSlots * 32 * G::stride + static_cast<size_t>(nw) * kD * 6 +
                              static_cast<size_t>(hpm) * 32 * cg * 4;
         auto k4 = decode_stage_look_kernel;
         e = cudaFuncSetAttribute(k4, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem4));
