@@ -125,6 +125,10 @@ typedef struct hp_stage_args {
     size_t workspace_bytes;
     hp_kv_view keys;
     hp_rope_ctx rope;
+    /* optional device flag (NULL = unknown): nonzero when every bf16 key is 0 or has
+     * |k| in [2^-63, 2^63], so bf16 q*k products are exact in fp32 and the sequential
+     * dot may run as one fused multiply-add per element (same result, fewer instructions) */
+    const int32_t* keys_exact;
 } hp_stage_args;
 
 size_t hp_stage_workspace_bytes(int32_t n_lists, int32_t max_chunks, int32_t keep, int32_t chunk_size);

@@ -60,7 +60,8 @@ class StageArgs(C.Structure):
                 ("max_chunks", C.c_int32), ("in_list", C.c_void_p), ("in_start", C.c_void_p),
                 ("in_count", C.c_void_p), ("in_stride", C.c_int64), ("out_list", C.c_void_p),
                 ("out_count", C.c_void_p), ("out_stride", C.c_int64), ("workspace", C.c_void_p),
-                ("workspace_bytes", C.c_size_t), ("keys", KvView), ("rope", RopeCtx)]
+                ("workspace_bytes", C.c_size_t), ("keys", KvView), ("rope", RopeCtx),
+                ("keys_exact", C.c_void_p)]
 
 
 class BsaArgs(C.Structure):

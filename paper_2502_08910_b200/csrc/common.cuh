@@ -199,6 +199,26 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
     return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
+// ---- exact-product dot helpers ---------------------------------------------------
+// fma(q, k, acc) rounds once, exactly like the reference's acc + (q*k) when the product
+// q*k is exact in fp32 (q and k bf16 with |x| in [2^-63, 2^63] or 0). fma.rn.f32.bf16
+// (SASS FHFMA.BF16) takes both operands as bf16 halves of packed pairs.
+__device__ __forceinline__ float fma_bf16(uint32_t a, uint32_t b, float c, bool hi) {
+    float d;
+    const uint16_t ah = static_cast<uint16_t>(hi ? a >> 16 : a & 0xffffu);
+    const uint16_t bh = static_cast<uint16_t>(hi ? b >> 16 : b & 0xffffu);
+    asm("fma.rn.f32.bf16 %0, %1, %2, %3;" : "=f"(d) : "h"(ah), "h"(bh), "f"(c));
+    return d;
+}
+
+// q is bf16-exact with |q| in [2^-63, 2^63] or 0 (so bf16 products stay exact).
+__device__ __forceinline__ bool q_product_safe(float x) {
+    const uint32_t u = __float_as_uint(x);
+    if ((u & 0xffffu) != 0u) return false;
+    const float ax = fabsf(x);
+    return ax == 0.0f || (ax >= 1.0842022e-19f && ax <= 9.2233720e18f);
+}
+
 // ---- last-CTA ticket ---------------------------------------------------------------
 // Called by all threads after the CTA's global writes. One thread takes the ticket
 // with a gpu-scope acq_rel atomic: release publishes every write the CTA made

@@ -99,13 +99,6 @@ __device__ __forceinline__ float dot_row<float>(const unsigned char* row, int sw
 // [2^-63, 2^63] or 0): fma(q, k, acc) then rounds once, exactly like the reference's
 // acc + (q*k). fma.rn.f32.bf16 (SASS FHFMA.BF16) takes both operands as bf16 halves,
 // so one instruction per element and no unpacking; qb holds q as packed bf16 pairs.
-__device__ __forceinline__ float fma_bf16(uint32_t a, uint32_t b, float c, bool hi) {
-    float d;
-    const uint16_t ah = static_cast<uint16_t>(hi ? a >> 16 : a & 0xffffu);
-    const uint16_t bh = static_cast<uint16_t>(hi ? b >> 16 : b & 0xffffu);
-    asm("fma.rn.f32.bf16 %0, %1, %2, %3;" : "=f"(d) : "h"(ah), "h"(bh), "f"(c));
-    return d;
-}
 __device__ __forceinline__ float dot_row_bf16x(const unsigned char* row, int swz, const uint32_t* qb) {
     const uint4* q4 = reinterpret_cast<const uint4*>(qb);
     float acc = 0.0f;
@@ -125,13 +118,6 @@ __device__ __forceinline__ float dot_row_bf16x(const unsigned char* row, int swz
     return acc;
 }
 
-// q is bf16-exact with |q| in [2^-63, 2^63] or 0 (so bf16 products stay exact).
-__device__ __forceinline__ bool q_product_safe(float x) {
-    const uint32_t u = __float_as_uint(x);
-    if ((u & 0xffffu) != 0u) return false;
-    const float ax = fabsf(x);
-    return ax == 0.0f || (ax >= 1.0842022e-19f && ax <= 9.2233720e18f);
-}
 
 template <typename T>
 __device__ __forceinline__ float elem(const unsigned char* row, int swz, int i) {

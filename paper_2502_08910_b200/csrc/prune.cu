@@ -108,6 +108,49 @@ __device__ __forceinline__ float block_score(const unsigned char* krow, const fl
     return best;
 }
 
+// σ with one FHFMA per element (keys certified and q bf16-exact: every product is
+// exact, so fma == the separately rounded multiply-add): the key row is held in
+// registers across the query rows, the packed q rows are shared-memory broadcasts.
+__device__ __forceinline__ float block_score_fma(const unsigned char* krow, const uint32_t* qb, int rows) {
+    uint4 k[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) k[c] = reinterpret_cast<const uint4*>(krow)[c];
+    float best = 0.0f;
+    int t = 0;
+    for (; t + 4 <= rows; t += 4) {  // four query rows as independent FHFMA chains
+        const uint4* q4 = reinterpret_cast<const uint4*>(qb + t * 64);
+        float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint4 q = q4[u * 16 + c];
+                acc[u] = fma_bf16(q.x, k[c].x, acc[u], false); acc[u] = fma_bf16(q.x, k[c].x, acc[u], true);
+                acc[u] = fma_bf16(q.y, k[c].y, acc[u], false); acc[u] = fma_bf16(q.y, k[c].y, acc[u], true);
+                acc[u] = fma_bf16(q.z, k[c].z, acc[u], false); acc[u] = fma_bf16(q.z, k[c].z, acc[u], true);
+                acc[u] = fma_bf16(q.w, k[c].w, acc[u], false); acc[u] = fma_bf16(q.w, k[c].w, acc[u], true);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (t + u == 0 || acc[u] > best) best = acc[u];  // rows in order, strict '>'
+    }
+    for (; t < rows; ++t) {
+        const uint4* q4 = reinterpret_cast<const uint4*>(qb + t * 64);
+        float acc = 0.0f;
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+            const uint4 q = q4[c];
+            acc = fma_bf16(q.x, k[c].x, acc, false); acc = fma_bf16(q.x, k[c].x, acc, true);
+            acc = fma_bf16(q.y, k[c].y, acc, false); acc = fma_bf16(q.y, k[c].y, acc, true);
+            acc = fma_bf16(q.z, k[c].z, acc, false); acc = fma_bf16(q.z, k[c].z, acc, true);
+            acc = fma_bf16(q.w, k[c].w, acc, false); acc = fma_bf16(q.w, k[c].w, acc, true);
+        }
+        if (t == 0 || acc > best) best = acc;
+    }
+    return best;
+}
+
 // Gather one key row per active lane (tok >= 0) of this warp into shared memory.
 template <typename T, int D>
 __device__ __forceinline__ void stage_rows(const hp_stage_args& a, int kv, int64_t tok,
@@ -164,10 +207,26 @@ __global__ void __launch_bounds__(256) prune_descent_kernel(const hp_stage_args 
     unsigned char* keys = smem + g.q_bytes + g.red_bytes;
 
     // rotate_queries (pruning.cpp:39-52): once per stage per head.
+    bool q_safe = true;
     for (int i = threadIdx.x; i < hpm * rows * d; i += blockDim.x) {
         const int hh = i / (rows * d), rem = i - hh * rows * d, t = rem / d, e = rem - t * d;
-        qs[(hh * g.rows_max + t) * d + e] =
-            a.q[(static_cast<int64_t>(m * hpm + hh) * a.q_rows + r0 + t) * d + e];
+        const float x = a.q[(static_cast<int64_t>(m * hpm + hh) * a.q_rows + r0 + t) * d + e];
+        qs[(hh * g.rows_max + t) * d + e] = x;
+        q_safe &= q_product_safe(x);
+    }
+    const bool all_safe = __syncthreads_and(q_safe);
+    // exact-product fast path: q rows re-packed as bf16 pairs over the fp32 copy
+    // ([head][row][64] words; the fp32 rows are not read again on this path)
+    const bool use_fma = !EXT && D == 128 && sizeof(T) == 2 && all_safe && a.keys_exact != nullptr &&
+                         *a.keys_exact != 0;
+    uint32_t* qb = reinterpret_cast<uint32_t*>(qs);
+    if (use_fma) {
+        for (int i = threadIdx.x; i < hpm * rows * 64; i += blockDim.x) {
+            const int hh = i / (rows * 64), rem = i - hh * rows * 64, t = rem >> 6, e = rem & 63;
+            const float2 x = *reinterpret_cast<const float2*>(
+                a.q + (static_cast<int64_t>(m * hpm + hh) * a.q_rows + r0 + t) * 128 + 2 * e);
+            qb[(hh * g.rows_max + t) * 64 + e] = (__float_as_uint(x.x) >> 16) | (__float_as_uint(x.y) & 0xffff0000u);
+        }
     }
     __syncthreads();
     if constexpr (EXT) {
@@ -195,6 +254,7 @@ __global__ void __launch_bounds__(256) prune_descent_kernel(const hp_stage_args 
     const int qh = m * hpm + hh;
     const int kv = qh / (a.n_q_heads / a.keys.n_kv);
     const float* qrows = qs + hh * g.rows_max * d;
+    const uint32_t* qbrows = qb + hh * g.rows_max * 64;
 
     const int64_t j = chunk0 + grp * 32 + lane;
     const bool active = j < cc;
@@ -221,6 +281,8 @@ __global__ void __launch_bounds__(256) prune_descent_kernel(const hp_stage_args 
         if constexpr (EXT) {
             s1 = block_score<T, D, true>(myrow, qrows, rows, d, cs1, sn1);
             s2 = same_rot ? s1 : block_score<T, D, true>(myrow, qrows, rows, d, cs2, sn2);
+        } else if (use_fma) {
+            if constexpr (D == 128 && sizeof(T) == 2) s1 = s2 = block_score_fma(myrow, qbrows, rows);
         } else {
             s1 = s2 = block_score<T, D, false>(myrow, qrows, rows, d, nullptr, nullptr);
         }

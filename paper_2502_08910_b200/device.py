@@ -202,7 +202,8 @@ def prune_stage(stage, q: torch.Tensor, kv: PagedKV, *, n_masks: int, n_blocks: 
                   max_chunks=max_chunks, in_list=_ptr(in_list), in_start=_ptr(in_start),
                   in_count=_ptr(in_count), in_stride=in_stride, out_list=_ptr(out_list),
                   out_count=_ptr(out_count), out_stride=out_list.shape[-1], workspace=_ptr(w),
-                  workspace_bytes=w.numel(), keys=kv.view(), rope=policy.ctx(layer1, rope))
+                  workspace_bytes=w.numel(), keys=kv.view(), rope=policy.ctx(layer1, rope),
+                  keys_exact=_ptr(getattr(kv, "keys_exact", None)))
     check(lib().hp_prune_stage(C.byref(a), C.c_void_p(_stream(stream))))
 
 
