@@ -11,10 +11,11 @@ synthetic Q/K/V (reference generator recipe, torch RNG). The amortized
 (16,8,4) stage-cache schedule ("Total") and the BSA-only step are reported
 alongside.
 
-Multi-GPU (torchrun, one process per GPU): weak scaling by KV-head group — every
-rank owns 8 (layer, KV-group) units, i.e. one layer's worth of groups, with no
-data-path collective. value = whole-job µs per layer =
-(max-over-ranks step time) / N.
+Multi-GPU (torchrun, one process per GPU): weak scaling over independent
+(layer, KV-group) units (groups never exchange data) — every
+rank runs the full 8-group step on its own L = 8 layers (64 units per GPU), no
+data-path collective. value = whole-job µs per layer = (max-over-ranks step time)
+/ (L x N).
 
 `--impl reference` times the reference's own CPU implementation of the same
 step (oracle/_ref, the unmodified reference library; the C port if it was not
@@ -68,7 +69,7 @@ def config(args, world):
                         f"(distinct KV per layer), reported per layer",
             "context": args.ctx, "q_heads": GROUPS * HPM, "kv_heads": GROUPS, "head_dim": D,
             "preset": "3k", "stages": STAGES, "sink": SINK, "stream": STREAM,
-            "units_per_gpu": f"{GROUPS} (layer, KV-group) units", "parallelism": f"kv-group x{world}",
+            "units_per_gpu": f"{GROUPS * args.layers} (layer, KV-group) units ({args.layers} layers x {GROUPS} groups)", "parallelism": f"kv-group x{world}",
             "layers_per_step": args.layers,
             "l2": "flushed before every timed step: 512 MB write, then 512 MB read (dirty lines evicted)"}
 
