@@ -297,6 +297,12 @@ typedef struct hp_decode_bsa_args {
     size_t workspace_bytes;
     hp_kv_view kv;
     hp_rope_ctx rope;
+    /* 1 = the mask lists/counts and every K/V row except the newest token's (position
+     * query_position) are already final when the launch is enqueued — no launch still in
+     * flight writes them (e.g. a step that reuses the cached last stage). The kernel then
+     * gathers those rows in its PDL prologue, overlapping the previous kernel's tail.
+     * Ignored with a page table (cached KV). 0 = wait first (always safe). */
+    int32_t mask_stable;
 } hp_decode_bsa_args;
 
 size_t hp_decode_bsa_workspace_bytes(int32_t n_q_heads, int32_t max_sel);

@@ -97,7 +97,8 @@ class DecodeBsaArgs(C.Structure):
                 ("query_position", C.c_int64), ("mask", ListRef), ("mask_count", C.c_void_p),
                 ("max_mask", C.c_int32), ("out", C.c_void_p), ("part_m", C.c_void_p),
                 ("part_l", C.c_void_p), ("part_o", C.c_void_p), ("workspace", C.c_void_p),
-                ("workspace_bytes", C.c_size_t), ("kv", KvView), ("rope", RopeCtx)]
+                ("workspace_bytes", C.c_size_t), ("kv", KvView), ("rope", RopeCtx),
+                ("mask_stable", C.c_int32)]
 
 
 class BsaPrefillArgs(C.Structure):

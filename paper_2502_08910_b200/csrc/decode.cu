@@ -1026,7 +1026,6 @@ template <typename T, int HC, bool EXT, int NT = kBsaThreads, int MK = kBsaMaxKe
 __global__ void __launch_bounds__(NT, 1)
 decode_bsa_kernel(const hp_decode_bsa_args a, float* part, int* tickets, int splits, int kpc) {
     pdl_trigger();
-    pdl_wait();
     constexpr int NQ = NT / 64;  // PV key groups of 32
     static_assert(MK / NQ == 32, "PV assumes 32 keys per group");
     using S = BsaSmem<T, HC, MK, NQ>;
@@ -1055,10 +1054,16 @@ decode_bsa_kernel(const hp_decode_bsa_args a, float* part, int* tickets, int spl
     const int64_t sink_end = min64(a.sink_tokens, pos + 1);
     int64_t stream_begin = pos + 1 > a.stream_tokens ? pos + 1 - a.stream_tokens : 0;
     stream_begin = max64(stream_begin, sink_end);
+    // PDL prologue: with a stable mask (resident KV) every row but the newest token's is
+    // final before this launch, so CTAs without the newest row gather before the wait
+    const bool early_ok = !EXT && a.mask_stable != 0 && a.kv.page_table == nullptr;
+    if (!early_ok) pdl_wait();
     const int64_t n_mask = a.mask_count[mask];
     const int64_t n_sel = sink_end + n_mask + (pos + 1 - stream_begin);
     const int64_t p0 = static_cast<int64_t>(split) * kpc;
     const int nv = static_cast<int>(max64(0, min64(kpc, n_sel - p0)));
+    const bool early = early_ok && p0 + nv < n_sel;  // the newest token (= last selected) is not here
+    if (early_ok && !early) pdl_wait();
     const float scale = 1.0f / sqrtf(static_cast<float>(kD));
 
     trace(2, 0);
@@ -1073,7 +1078,6 @@ decode_bsa_kernel(const hp_decode_bsa_args a, float* part, int* tickets, int spl
         vptr[t] = reinterpret_cast<unsigned long long>(kv_row_ptr(a.kv, a.kv.v_pool, a.kv.v_host, kvh, tok, sizeof(T)));
     }
     if (cut == 5) return;
-    for (int i = t; i < HC * kD; i += NT) qs[i] = a.q[static_cast<int64_t>(h0) * kD + i];
     __syncthreads();
     if (cut == 6) return;
     {
@@ -1095,6 +1099,8 @@ decode_bsa_kernel(const hp_decode_bsa_args a, float* part, int* tickets, int spl
         }
         cp_async_commit();
     }
+    if (early) pdl_wait();  // q (and everything after) is the preceding launch's to write
+    for (int i = t; i < HC * kD; i += NT) qs[i] = a.q[static_cast<int64_t>(h0) * kD + i];
     if constexpr (EXT) {  // q at its true position (sparse_attention.cpp:47)
         __syncthreads();
         const float* cs = a.rope.cos_tab + pos * half;

@@ -522,7 +522,9 @@ class FusedDecodeLayer:
             mask=chains[-1], mask_count=_ptr(self.count[-1]), max_mask=self.stages[-1][2],
             out=_ptr(self.out), part_m=None, part_l=None, part_o=None,
             workspace=_ptr(self.ws_bsa), workspace_bytes=self.ws_bsa.numel(), kv=kvv,
-            rope=self.policy.ctx(0, self.rope))
+            rope=self.policy.ctx(0, self.rope),
+            # the last stage's cache is untouched this step: gather in the PDL prologue
+            mask_stable=0 if refresh[-1] else 1)
         check(lib().hp_decode_bsa(C.byref(b), sp))
         if materialize:
             idx = [i for i in range(S - 1) if refresh[i]]  # the last stage wrote its own

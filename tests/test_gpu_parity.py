@@ -292,6 +292,11 @@ def test_fused_decode_layer_step(port, case):
             got = cl[g, : int(cc[g])].cpu().numpy()
             assert np.array_equal(got, masks[g]), g
         assert_close(out.cpu().numpy().reshape(groups, hpm, 128), want_out)
+    # a step that reuses every cache gathers in the BSA's PDL prologue (mask_stable):
+    # same mask, same output
+    out2 = layer.run(t, refresh=[False] * 3).clone()
+    torch.cuda.synchronize()
+    assert torch.equal(out2, out)
 
 
 def test_fused_decode_refresh_schedule():
