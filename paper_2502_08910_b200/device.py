@@ -462,7 +462,15 @@ class FusedDecodeLayer:
         self.count = [torch.zeros((n_masks,), dtype=torch.int32, device=dev) for _ in range(S)]
         self.cache = [torch.zeros((n_masks, keep), dtype=torch.int32, device=dev)
                       for (_, _, keep) in self.stages]
-        self.q = torch.zeros((n_q_heads, kv.d), dtype=torch.float32, device=dev)
+        # q and the new token's K/V rows share one device buffer so the host-facing call
+        # (step_host) moves all of a step's inputs with a single H2D copy
+        esz = torch.tensor([], dtype=kv.dtype).element_size()
+        self._io_q = n_q_heads * kv.d * 4
+        self._io_kv = kv.n_kv * kv.d * esz
+        self._d_io = torch.zeros(self._io_q + 2 * self._io_kv, dtype=torch.uint8, device=dev)
+        self.q = self._d_io[: self._io_q].view(torch.float32).view(n_q_heads, kv.d)
+        self._d_k = self._d_io[self._io_q: self._io_q + self._io_kv].view(kv.dtype).view(kv.n_kv, kv.d)
+        self._d_v = self._d_io[self._io_q + self._io_kv:].view(kv.dtype).view(kv.n_kv, kv.d)
         self.out = torch.zeros((n_q_heads, kv.d), dtype=torch.float32, device=dev)
         t_max = kv.num_pages * kv.page_size
         n0 = max(0, t_max - stream_tokens - sink)
@@ -576,14 +584,13 @@ class FusedDecodeLayer:
         has_kv = k_row is not None
         key = (t, tuple(refresh) if refresh is not None else None, has_kv)
         if not hasattr(self, "_hg"):
-            dev = self.dev
             self._hg = {}
-            self._h_q = torch.empty((self.n_q_heads, self.kv.d), dtype=torch.float32).pin_memory()
-            self._h_k = torch.empty((self.kv.n_kv, self.kv.d), dtype=self.kv.dtype).pin_memory()
-            self._h_v = torch.empty((self.kv.n_kv, self.kv.d), dtype=self.kv.dtype).pin_memory()
+            self._h_io = torch.empty(self._d_io.numel(), dtype=torch.uint8).pin_memory()
+            self._h_q = self._h_io[: self._io_q].view(torch.float32).view(self.q.shape)
+            self._h_k = self._h_io[self._io_q: self._io_q + self._io_kv].view(self.kv.dtype).view(self._d_k.shape)
+            self._h_v = self._h_io[self._io_q + self._io_kv:].view(self.kv.dtype).view(self._d_v.shape)
             self._h_out = torch.empty((self.n_q_heads, self.kv.d), dtype=torch.float32).pin_memory()
-            self._d_k = torch.empty((self.kv.n_kv, self.kv.d), dtype=self.kv.dtype, device=dev)
-            self._d_v = torch.empty((self.kv.n_kv, self.kv.d), dtype=self.kv.dtype, device=dev)
+            self._side = torch.cuda.Stream(device=self.dev)
         self._h_q.copy_(torch.as_tensor(q_host).reshape(self._h_q.shape))
         if has_kv:
             self._h_k.copy_(torch.as_tensor(k_row).reshape(self._h_k.shape))
@@ -591,16 +598,20 @@ class FusedDecodeLayer:
         g = self._hg.get(key)
         if g is None:
             def body():
-                self.q.copy_(self._h_q, non_blocking=True)
+                # one H2D copy of q + the token's K/V rows, append, the layer step (stage
+                # caches materialized on a side branch), one D2H copy of the output
+                cur = torch.cuda.current_stream()
+                n_in = self._d_io.numel() if has_kv else self._io_q
+                self._d_io[:n_in].copy_(self._h_io[:n_in], non_blocking=True)
                 if has_kv:
-                    self._d_k.copy_(self._h_k, non_blocking=True)
-                    self._d_v.copy_(self._h_v, non_blocking=True)
                     view = self.kv.view(t)
                     check(lib().hp_decode_append(C.byref(view), _ptr(self._d_k), _ptr(self._d_v),
                                                  t - 1, _ptr(self.kv.keys_exact),
                                                  C.c_void_p(_stream())))
-                self.run(t, refresh=refresh)
+                self._side.wait_stream(cur)
+                self.run(t, refresh=refresh, mat_stream=self._side)
                 self._h_out.copy_(self.out, non_blocking=True)
+                cur.wait_stream(self._side)
             s = torch.cuda.Stream(device=self.dev)
             s.wait_stream(torch.cuda.current_stream())
             with torch.cuda.stream(s):

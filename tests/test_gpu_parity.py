@@ -339,3 +339,32 @@ def test_fused_decode_refresh_schedule():
                 assert torch.equal(fl[g, :n].cpu(), gl[g, 0, :n].cpu()), (s, i, g)
         assert_close(of.cpu().numpy(), og[:, 0].cpu().numpy(), rtol=1e-5)
         counters = [(c + 1) % iv for c, iv in zip(counters, intervals)]
+
+
+def test_fused_step_host_matches_device_path():
+    """The host-facing per-layer call (pinned q/K/V in, one H2D copy, append, step with
+    side-branch caches, one D2H copy) equals the device path driven step by step."""
+    D = _dev()
+    dev = torch.device("cuda")
+    stages = [(1, 64, 4096), (1, 16, 1024), (1, 4, 256)]
+    t0, steps, groups, hpm = 40000, 4, 2, 4
+    q, k, v = workload(13, groups * hpm, groups, steps, t0 + steps, 128, bf16=True)
+    kw = dict(sink=64, stream_tokens=256, n_q_heads=groups * hpm, n_masks=groups)
+    kv1 = D.PagedKV(torch.from_numpy(k[:, :t0]), torch.from_numpy(v[:, :t0]), dtype=torch.bfloat16,
+                    capacity=t0 + steps)
+    kv2 = D.PagedKV(torch.from_numpy(k[:, :t0]), torch.from_numpy(v[:, :t0]), dtype=torch.bfloat16,
+                    capacity=t0 + steps)
+    host = D.FusedDecodeLayer(kv1, stages, **kw)
+    ref = D.FusedDecodeLayer(kv2, stages, **kw)
+    for s in range(steps):
+        t = t0 + s + 1
+        flags = [s % 2 == 0, True, s % 2 == 0]
+        got = host.step_host(t, q[:, s], k[:, t - 1], v[:, t - 1], refresh=flags).clone()
+        kv2.append(torch.from_numpy(k[:, t - 1]).to(dev, torch.bfloat16),
+                   torch.from_numpy(v[:, t - 1]).to(dev, torch.bfloat16))
+        ref.q.copy_(torch.from_numpy(q[:, s]).to(dev))
+        want = ref.run(t, refresh=flags).cpu()
+        torch.cuda.synchronize()
+        assert torch.equal(got, want), s
+        for i in range(3):
+            assert torch.equal(host.mask(i)[1], ref.mask(i)[1])
