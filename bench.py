@@ -184,11 +184,15 @@ def main():
     import torch
     from paper_2502_08910_b200 import device as D_, synth
 
+    # one GPU per rank; HP_BENCH_BACKEND=gloo + fewer GPUs than ranks is a dev check of the
+    # multi-rank logic on a 1-GPU box (ranks then share a device)
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("HP_BENCH_BACKEND", "nccl")
+        dist.init_process_group(backend, **({"device_id": dev} if backend == "nccl" else {}))
     D_.require_cuda()
 
     t = args.ctx
