@@ -133,6 +133,12 @@ __device__ __forceinline__ void progress(int code) {
     }
 }
 
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 struct PrefillSmem {
     static constexpr uint32_t tile_bytes = kTN * kHD * 2;  // 32 KB
     static constexpr uint32_t q_off = 0;
@@ -240,7 +246,8 @@ __global__ void __launch_bounds__(kThreads, 1) bsa_prefill_tc_kernel(const hp_bs
     const bool my_ok = my_r < rows_here;
     const int64_t my_pos = pos_first + (my_ok ? my_r : rows_here - 1);
     const int64_t my_sb = stream_begin(my_pos);
-    const float scale = 1.0f / sqrtf(static_cast<float>(kHD));
+    // softmax in base 2: scores scaled by log2(e)/sqrt(d), exponentials on MUFU.EX2
+    const float scale = 1.4426950408889634f / sqrtf(static_cast<float>(kHD));
     float run_m = -INFINITY, run_l = 0.f;  // run_l: this thread's half of the row sum
     const uint32_t lane_base = static_cast<uint32_t>((w & 3) * 32) << 16;
     const uint32_t tS = tmem + lane_base + half * 64;        // this half's S columns
@@ -305,24 +312,31 @@ __global__ void __launch_bounds__(kThreads, 1) bsa_prefill_tc_kernel(const hp_bs
         float sv[kTN / 2];
 #pragma unroll
         for (int c = 0; c < kTN / 64; ++c) tmem_ld32(tS + c * 32, sv + c * 32);
-        float tmax = -INFINITY;
+        // selection test, branch-free (union entries past U read as 0x7fffffff = never
+        // selected); four independent max chains
+        float tm4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        const int ub = tile * kTN + half * 64;
+        const int32_t pos32 = my_ok ? static_cast<int32_t>(my_pos) : -1;
+        const int32_t sb32 = static_cast<int32_t>(my_sb), sink32 = static_cast<int32_t>(min64(sink, 0x7fffffff));
 #pragma unroll
         for (int jj = 0; jj < kTN / 2; ++jj) {
-            const int ui = tile * kTN + half * 64 + jj;
-            bool ok = ui < U && my_ok;
-            if (ok) {
-                const int32_t e = uni[ui];
-                const int64_t u = e & 0x7fffffff;
-                ok = u <= my_pos && (u < sink || e < 0 || u >= my_sb);
-            }
+            const int32_t e = (ub + jj < U) ? uni[ub + jj] : 0x7fffffff;
+            const int32_t u = e & 0x7fffffff;
+            const bool ok = u <= pos32 && (u < sink32 || e < 0 || u >= sb32);
             sv[jj] = ok ? sv[jj] * scale : -INFINITY;
-            tmax = fmaxf(tmax, sv[jj]);
+            tm4[jj & 3] = fmaxf(tm4[jj & 3], sv[jj]);
         }
+        const float tmax = fmaxf(fmaxf(tm4[0], tm4[1]), fmaxf(tm4[2], tm4[3]));
         sh_max[half][my_i] = tmax;
         __syncthreads();
-        const float new_m = fmaxf(run_m, fmaxf(sh_max[0][my_i], sh_max[1][my_i]));
-        const float alpha = (run_m == -INFINITY) ? 0.f : expf(run_m - new_m);
-        float psum = 0.f;
+        // lazy rescale (base 2): keep a stale running max unless the tile's max exceeds it
+        // by more than 2^8 — P (bf16) and the fp32 sums stay in range, O and l share the
+        // same reference, so the final O / l is unchanged; most tiles skip the TMEM rescale
+        const float tile_m = fmaxf(sh_max[0][my_i], sh_max[1][my_i]);
+        const float new_m = (run_m != -INFINITY && tile_m <= run_m + 8.0f) ? run_m : fmaxf(run_m, tile_m);
+        const float alpha = (run_m == -INFINITY) ? 0.f : ex2_approx(run_m - new_m);
+        float ps4[4] = {0.f, 0.f, 0.f, 0.f};
+        const float mref = new_m == -INFINITY ? 0.f : new_m;  // rows with nothing selected yet: all p = 0
         unsigned char* ps = smem + S::p_off;
 #pragma unroll
         for (int c = 0; c < kTN / 16; ++c) {
@@ -330,12 +344,13 @@ __global__ void __launch_bounds__(kThreads, 1) bsa_prefill_tc_kernel(const hp_bs
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 const float x = sv[c * 8 + u];
-                p[u] = (x == -INFINITY) ? 0.f : expf(x - new_m);
-                psum += p[u];
+                p[u] = ex2_approx(x - mref);  // masked: ex2(-inf) = 0
+                ps4[u & 3] += p[u];
             }
             *reinterpret_cast<uint4*>(ps + kmajor_off(my_i, half * 64 + c * 8)) =
                 make_uint4(pack_bf16(p[0], p[1]), pack_bf16(p[2], p[3]), pack_bf16(p[4], p[5]), pack_bf16(p[6], p[7]));
         }
+        const float psum = (ps4[0] + ps4[1]) + (ps4[2] + ps4[3]);
         run_l = run_l * alpha + psum;
         run_m = new_m;
         // tcgen05.ld/st are .sync.aligned: the whole warp rescales if any row needs it
