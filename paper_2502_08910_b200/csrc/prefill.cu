@@ -257,6 +257,14 @@ __global__ void __launch_bounds__(kThreads, 1) bsa_prefill_tc_kernel(const hp_bs
     const uint32_t sbase = smem_u32(smem);
     const int n_tiles = (U + kTN - 1) / kTN;
     __shared__ float sh_max[2][kTM];
+    // resident KV with power-of-two pages: a row is pool + 256 B x (page*n_kv + kvh)*ps + off,
+    // 32-bit index math (rows < 2^32) instead of the general page-table walk
+    const uint32_t ps = static_cast<uint32_t>(a.kv.page_size);
+    const bool fast_rows = a.kv.page_table == nullptr && a.kv.touched == nullptr && a.kv.row_bits == nullptr &&
+                           (ps & (ps - 1)) == 0 &&
+                           static_cast<uint64_t>(a.kv.num_pages) * a.kv.n_kv * ps < (1ull << 32);
+    const uint32_t ps_shift = static_cast<uint32_t>(__ffs(static_cast<int>(ps)) - 1);
+    const uint32_t nkv = static_cast<uint32_t>(a.kv.n_kv);
     // coalesced gather: 16 threads per 256 B row (one 16 B chunk each), 16 rows per pass
     auto gather = [&](int tile, int buf) {
         unsigned char* ks = smem + S::k_off + buf * S::tile_bytes;
@@ -267,9 +275,17 @@ __global__ void __launch_bounds__(kThreads, 1) bsa_prefill_tc_kernel(const hp_bs
             const int j = j0 + (t >> 4);
             const int ui = tile * kTN + j;
             if (ui < U) {
-                const int64_t tok = uni[ui] & 0x7fffffff;
-                const char* kp = kv_row_ptr(a.kv, a.kv.k_pool, a.kv.k_host, kvh, tok, 2);
-                const char* vp = kv_row_ptr(a.kv, a.kv.v_pool, a.kv.v_host, kvh, tok, 2);
+                const uint32_t tk = static_cast<uint32_t>(uni[ui]) & 0x7fffffffu;
+                const char* kp;
+                const char* vp;
+                if (fast_rows) {
+                    const uint32_t idx = (((tk >> ps_shift) * nkv + static_cast<uint32_t>(kvh)) << ps_shift) + (tk & (ps - 1));
+                    kp = static_cast<const char*>(a.kv.k_pool) + static_cast<size_t>(idx) * (kHD * 2);
+                    vp = static_cast<const char*>(a.kv.v_pool) + static_cast<size_t>(idx) * (kHD * 2);
+                } else {
+                    kp = kv_row_ptr(a.kv, a.kv.k_pool, a.kv.k_host, kvh, tk, 2);
+                    vp = kv_row_ptr(a.kv, a.kv.v_pool, a.kv.v_host, kvh, tk, 2);
+                }
                 cp_async16(ks + kmajor_off(j, c * 8), kp + c * 16);
                 cp_async16(vs + mnmajor_off(j, c * 8), vp + c * 16);
             } else {
@@ -319,12 +335,18 @@ __global__ void __launch_bounds__(kThreads, 1) bsa_prefill_tc_kernel(const hp_bs
         const int32_t pos32 = my_ok ? static_cast<int32_t>(my_pos) : -1;
         const int32_t sb32 = static_cast<int32_t>(my_sb), sink32 = static_cast<int32_t>(min64(sink, 0x7fffffff));
 #pragma unroll
-        for (int jj = 0; jj < kTN / 2; ++jj) {
-            const int32_t e = (ub + jj < U) ? uni[ub + jj] : 0x7fffffff;
-            const int32_t u = e & 0x7fffffff;
-            const bool ok = u <= pos32 && (u < sink32 || e < 0 || u >= sb32);
-            sv[jj] = ok ? sv[jj] * scale : -INFINITY;
-            tm4[jj & 3] = fmaxf(tm4[jj & 3], sv[jj]);
+        for (int j4 = 0; j4 < kTN / 2; j4 += 4) {  // four union entries per 16-byte load
+            const int4 e4 = *reinterpret_cast<const int4*>(uni + ub + j4);
+            const int32_t ev[4] = {e4.x, e4.y, e4.z, e4.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int jj = j4 + q;
+                const int32_t e = (ub + jj < U) ? ev[q] : 0x7fffffff;
+                const int32_t u = e & 0x7fffffff;
+                const bool ok = u <= pos32 && (u < sink32 || e < 0 || u >= sb32);
+                sv[jj] = ok ? sv[jj] * scale : -INFINITY;
+                tm4[q] = fmaxf(tm4[q], sv[jj]);
+            }
         }
         const float tmax = fmaxf(fmaxf(tm4[0], tm4[1]), fmaxf(tm4[2], tm4[3]));
         sh_max[half][my_i] = tmax;
@@ -417,7 +439,8 @@ extern "C" int hp_debug_prefill_progress(int* mapped_word) {
 }
 
 extern "C" size_t hp_bsa_prefill_smem_bytes(int32_t max_union) {
-    return PrefillSmem::u_off + static_cast<size_t>(max_union) * 4;
+    // union list padded to whole 128-key tiles: the selection test reads it 16 bytes at a time
+    return PrefillSmem::u_off + static_cast<size_t>((max_union + kTN - 1) / kTN * kTN) * 4;
 }
 
 extern "C" int hp_bsa_prefill(const hp_bsa_prefill_args* ap, void* stream) {
