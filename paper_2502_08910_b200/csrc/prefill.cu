@@ -334,6 +334,12 @@ __global__ void __launch_bounds__(kThreads, 1) bsa_prefill_tc_kernel(const hp_bs
         const int ub = tile * kTN + half * 64;
         const int32_t pos32 = my_ok ? static_cast<int32_t>(my_pos) : -1;
         const int32_t sb32 = static_cast<int32_t>(my_sb), sink32 = static_cast<int32_t>(min64(sink, 0x7fffffff));
+        if (my_ok && ub + kTN / 2 <= s0 + nmid) {
+            // sinks and mask entries (union index < s0 + nmid) precede every row of the
+            // block (< stream_begin(first row)): all selected, no per-entry test
+#pragma unroll
+            for (int jj = 0; jj < kTN / 2; ++jj) tm4[jj & 3] = fmaxf(tm4[jj & 3], sv[jj]);
+        } else {
 #pragma unroll
         for (int j4 = 0; j4 < kTN / 2; j4 += 4) {  // four union entries per 16-byte load
             const int4 e4 = *reinterpret_cast<const int4*>(uni + ub + j4);
@@ -344,11 +350,12 @@ __global__ void __launch_bounds__(kThreads, 1) bsa_prefill_tc_kernel(const hp_bs
                 const int32_t e = (ub + jj < U) ? ev[q] : 0x7fffffff;
                 const int32_t u = e & 0x7fffffff;
                 const bool ok = u <= pos32 && (u < sink32 || e < 0 || u >= sb32);
-                sv[jj] = ok ? sv[jj] * scale : -INFINITY;
+                sv[jj] = ok ? sv[jj] : -INFINITY;  // raw scores; the scale is folded into the exponent
                 tm4[q] = fmaxf(tm4[q], sv[jj]);
             }
         }
-        const float tmax = fmaxf(fmaxf(tm4[0], tm4[1]), fmaxf(tm4[2], tm4[3]));
+        }
+        const float tmax = fmaxf(fmaxf(tm4[0], tm4[1]), fmaxf(tm4[2], tm4[3])) * scale;
         sh_max[half][my_i] = tmax;
         __syncthreads();
         // lazy rescale (base 2): keep a stale running max unless the tile's max exceeds it
@@ -366,7 +373,7 @@ __global__ void __launch_bounds__(kThreads, 1) bsa_prefill_tc_kernel(const hp_bs
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 const float x = sv[c * 8 + u];
-                p[u] = ex2_approx(x - mref);  // masked: ex2(-inf) = 0
+                p[u] = ex2_approx(fmaf(x, scale, -mref));  // masked: ex2(-inf) = 0
                 ps4[u & 3] += p[u];
             }
             *reinterpret_cast<uint4*>(ps + kmajor_off(my_i, half * 64 + c * 8)) =
