@@ -622,12 +622,7 @@ decode_stage_wide_kernel(const hp_decode_stage_args a, float* hscores, int group
     const int qh = m * hpm + hh;
     const int kvh = qh / (a.n_q_heads / a.keys.n_kv);
     const float* qrow = a.q + static_cast<int64_t>(qh) * kD;
-    // FFMA when every product is exact (bf16-exact q, keys certified), FMUL+FADD otherwise
-    bool q_safe = true;
-#pragma unroll
-    for (int i = 0; i < kD / 32; ++i) q_safe &= q_product_safe(__ldg(qrow + i * 32 + lane));
-    const bool use_fma = __all_sync(0xffffffffu, q_safe) && sizeof(T) == 2 && a.keys_exact != nullptr &&
-                         *a.keys_exact != 0;
+    bool use_fma = false;  // set below, while the first rows are in flight
     unsigned char* wstage = smem + static_cast<size_t>(w) * 32 * G::stride;
     const unsigned char* myrow = wstage + lane * G::stride;
     const int swz = lane & (G::bytes / 16 - 1);
@@ -677,7 +672,17 @@ decode_stage_wide_kernel(const hp_decode_stage_args a, float* hscores, int group
     int first = 1, last = len, it = 0, iters = 0;
     while ((1 << iters) < len) ++iters;
     float s1 = 0.f;
-    stage_rows<T>(a.keys, kvh, active ? token(0) : -1, wstage, lane);
+    stage_rows<T, false>(a.keys, kvh, active ? token(0) : -1, wstage, lane);
+    {
+        // FFMA when every product is exact (bf16-exact q, keys certified), FMUL+FADD
+        // otherwise — checked while the first gather is in flight
+        bool q_safe = true;
+#pragma unroll
+        for (int i = 0; i < kD / 32; ++i) q_safe &= q_product_safe(__ldg(qrow + i * 32 + lane));
+        use_fma = __all_sync(0xffffffffu, q_safe) && sizeof(T) == 2 && a.keys_exact != nullptr && *a.keys_exact != 0;
+    }
+    cp_async_wait_all();
+    __syncwarp();
     if (active) s1 = score();
     for (;;) {
         const bool go = active && it < iters && first < last;
