@@ -368,3 +368,27 @@ def test_fused_step_host_matches_device_path():
         assert torch.equal(got, want), s
         for i in range(3):
             assert torch.equal(host.mask(i)[1], ref.mask(i)[1])
+
+
+@pytest.mark.parametrize("t", [1, 7, 300, 1281, 1300, 2049, 5000, 40001])
+def test_fused_decode_short_and_ragged_contexts(port, t):
+    """Edge contexts on the fused path (3k preset): shorter than the sinks, shorter than
+    sink + stream (empty middle), a middle shorter than one stage-1 chunk, ragged last
+    pages and chunks — masks exact, outputs within 1e-3 of the oracle's decode body."""
+    D = _dev()
+    dev = torch.device("cuda")
+    stages = [(64, 256, 32768), (64, 32, 8192), (64, 8, 2048)]
+    groups, hpm = 2, 4
+    q, k, v = workload(17 + t, groups * hpm, groups, 1, t, 128, bf16=True)
+    kv = D.PagedKV(torch.from_numpy(k), torch.from_numpy(v), page_size=64, dtype=torch.bfloat16)
+    layer = D.FusedDecodeLayer(kv, stages, sink=256, stream_tokens=1024, n_q_heads=groups * hpm,
+                               n_masks=groups)
+    layer.q.copy_(torch.from_numpy(q[:, 0]).to(dev))
+    out = layer.run(t).clone()
+    torch.cuda.synchronize()
+    masks, want_out, _ = port.decode_layer_step(q.reshape(groups, hpm, 128), k, v, stages, sink=256,
+                                                stream=1024, ext=False, layer1=4)
+    cl, cc = layer.mask()
+    for g in range(groups):
+        assert np.array_equal(cl[g, : int(cc[g])].cpu().numpy(), masks[g]), g
+    assert_close(out.cpu().numpy().reshape(groups, hpm, 128), want_out)
