@@ -106,12 +106,13 @@ def test_host_logic_over_gloo_world2():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world", [2, 4, 8])
-def test_sharded_decode_matches_unsharded(world):
+@pytest.mark.parametrize("world,groups,t", [(2, 8, 1 << 18), (4, 8, 1 << 18), (8, 8, 1 << 18),
+                                           (8, 1, 3 << 20)])  # last: the C5 context (3M) of one KV group
+def test_sharded_decode_matches_unsharded(world, groups, t):
     from paper_2502_08910_b200 import _capi, device as D, synth
     import ctypes as C
     D.require_cuda()
-    groups, hpm, t, d = 8, 4, 1 << 18, 128
+    hpm, d = 4, 128
     stages = [(64, 256, 32768), (64, 32, 8192), (64, 8, 2048)]
     q, k, v = synth.generate(groups * hpm, groups, t, d, t_q=2, seed=9)
     full = D.FusedDecodeLayer(D.PagedKV(k, v), stages, sink=256, stream_tokens=1024,
