@@ -392,3 +392,44 @@ def test_fused_decode_short_and_ragged_contexts(port, t):
     for g in range(groups):
         assert np.array_equal(cl[g, : int(cc[g])].cpu().numpy(), masks[g]), g
     assert_close(out.cpu().numpy().reshape(groups, hpm, 128), want_out)
+
+
+def test_descent_reads_the_reference_rows(ref):
+    """acceptance #5 (acceptance.cpp:146-217) at 1M: the one-wave stage-1 kernel reads
+    exactly as many distinct key rows per KV group as the reference's instrumented
+    DirectKeySource (the descent never re-reads a scored row, and it never speculates),
+    which is what makes bench.py's row_bits count the algorithmic bytes. The latency-bound
+    stages 2/3 deliberately read more (both candidate next rows / whole short chunks)."""
+    from paper_2502_08910_b200 import synth
+    D = _dev()
+    stages = [(64, 256, 32768), (64, 32, 8192), (64, 8, 2048)]
+    t, groups, hpm = 1 << 20, 8, 4
+    q, k, v = synth.generate(groups * hpm, groups, t, 128, seed=29)
+    kv = D.PagedKV(k, v, page_size=64, dtype=torch.bfloat16)
+    layer = D.FusedDecodeLayer(kv, stages, sink=256, stream_tokens=1024, n_q_heads=groups * hpm,
+                               n_masks=groups)
+    layer.q.copy_(q[:, 0])
+    layer.run(t)  # materialized caches: each stage below reads its predecessor's list
+    torch.cuda.synchronize()
+    stride = kv.num_pages * kv.page_size
+
+    def per_group_rows():
+        bits = kv.row_bits.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+        cnt = torch.zeros_like(bits)
+        for sh in range(32):
+            cnt += (bits >> sh) & 1
+        words = stride // 32
+        return [int(cnt[g * words:(g + 1) * words].sum()) for g in range(groups)]
+
+    got = []
+    for i in range(3):
+        kv.count_rows(True)
+        layer.run_stage(t, i, select=False)
+        torch.cuda.synchronize()
+        got.append(per_group_rows())
+        kv.count_rows(False)
+    for g in (0, groups - 1):
+        want_dis, _ = ref.decode_read_counts(q[g * hpm:(g + 1) * hpm, 0].cpu().numpy(),
+                                             k[g].float().cpu().numpy(), stages, sink=256, stream=1024)
+        assert got[0][g] == int(want_dis[0]), (g, got[0][g], int(want_dis[0]))
+        assert got[1][g] >= int(want_dis[1]) and got[2][g] >= int(want_dis[2])
