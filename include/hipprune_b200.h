@@ -269,6 +269,13 @@ typedef struct hp_decode_stage_args {
 size_t hp_decode_stage_workspace_bytes(int32_t n_masks, int32_t max_chunks);
 int hp_decode_stage(const hp_decode_stage_args* args, void* stream);
 
+/* Which descent kernel hp_decode_stage launches for these arguments (host-only query,
+ * no launch): the one-wave kernel for big stages (>= ~2K warps of descents), all-rows
+ * for l_c <= 8, the two-comparison lookahead kernel for other bf16 stages, the classic
+ * one-row-per-round kernel otherwise (and whenever RoPE extension is on). */
+enum hp_stage_variant { HP_STAGE_CLASSIC = 0, HP_STAGE_LOOKAHEAD = 1, HP_STAGE_WIDE = 2, HP_STAGE_ALLROWS = 3 };
+int hp_decode_stage_variant(const hp_decode_stage_args* args, int32_t* variant);
+
 /* The stage's chunk selection on its own (run_pruning_stage's stable top-K,
  * pruning.cpp:187-192): per mask, keep the keep/chunk_size best of ceil(n_in/chunk_size)
  * scores (score desc, chunk asc), kept chunk ids ascending in sel_out, the stage output
@@ -307,6 +314,12 @@ typedef struct hp_decode_bsa_args {
 
 size_t hp_decode_bsa_workspace_bytes(int32_t n_q_heads, int32_t max_sel);
 int hp_decode_bsa(const hp_decode_bsa_args* args, void* stream);
+
+/* Which BSA kernel hp_decode_bsa launches for these arguments (validates them, no launch;
+ * queries the device's cluster occupancy): the thread-block-cluster kernel merging over
+ * distributed shared memory, or the split-K kernel whose last CTA merges (ticket). */
+enum hp_bsa_variant { HP_BSA_TICKET = 0, HP_BSA_CLUSTER = 1 };
+int hp_decode_bsa_variant(const hp_decode_bsa_args* args, int32_t* variant);
 
 /* Append one token's K/V rows (DecodeEngine::step, decode.cpp:202-208): rows
  * [n_kv][d] (same dtype as the pools) land at `token` of the paged pools; keys_exact

@@ -19,6 +19,8 @@ if os.environ.get("HP_LIB"):  # dev: an alternative build of the kernel library 
 HP_OK = 0
 HP_F32, HP_BF16 = 0, 1
 HP_ROPE_CHUNK_INDEXED, HP_ROPE_RELATIVE, HP_ROPE_STREAMING = 0, 1, 2
+STAGE_VARIANTS = {0: "classic", 1: "lookahead", 2: "wide", 3: "allrows"}  # hp_stage_variant
+BSA_VARIANTS = {0: "ticket", 1: "cluster"}  # hp_bsa_variant
 
 
 class ContractViolation(RuntimeError):
@@ -124,7 +126,7 @@ EXPORTS = ["hp_last_error", "hp_version", "hp_device_available", "hp_build_rope_
            "hp_stage_workspace_bytes", "hp_prune_stage", "hp_remap_blocks",
            "hp_selected_indices", "hp_bsa_workspace_bytes", "hp_bsa", "hp_lse_merge",
            "hp_decode_stage_workspace_bytes", "hp_decode_stage", "hp_decode_bsa_workspace_bytes",
-           "hp_decode_bsa", "hp_decode_materialize", "hp_decode_append", "hp_trace_enable", "hp_debug_cut",
+           "hp_decode_bsa", "hp_decode_stage_variant", "hp_decode_bsa_variant", "hp_decode_materialize", "hp_decode_append", "hp_trace_enable", "hp_debug_cut",
            "hp_cache_workspace_bytes", "hp_cache_commit", "hp_select_topk",
            "hp_bsa_prefill_smem_bytes", "hp_bsa_prefill", "hp_debug_prefill_progress"]
 
@@ -167,6 +169,10 @@ def lib():
     L.hp_decode_bsa_workspace_bytes.argtypes = [C.c_int32, C.c_int32]
     L.hp_decode_bsa.restype = C.c_int
     L.hp_decode_bsa.argtypes = [C.POINTER(DecodeBsaArgs), C.c_void_p]
+    L.hp_decode_stage_variant.restype = C.c_int
+    L.hp_decode_stage_variant.argtypes = [C.POINTER(DecodeStageArgs), C.POINTER(C.c_int32)]
+    L.hp_decode_bsa_variant.restype = C.c_int
+    L.hp_decode_bsa_variant.argtypes = [C.POINTER(DecodeBsaArgs), C.POINTER(C.c_int32)]
     L.hp_decode_materialize.restype = C.c_int
     L.hp_decode_materialize.argtypes = [C.POINTER(ListRef), C.POINTER(C.c_void_p),
                                         C.POINTER(C.c_void_p), C.POINTER(C.c_int64), C.c_int32,

@@ -1393,6 +1393,25 @@ int bsa_hc(int n_q_heads, int n_kv, int hpm) {
     return std::max(1, hc);
 }
 
+// Which descent kernel a stage launch takes (hp_decode_stage_variant): the one-wave
+// kernel for big stages, all-rows for short chunks, lookahead for latency-bound bf16
+// descents, the classic kernel otherwise (and always with RoPE extension).
+int stage_variant(const hp_decode_stage_args& a, size_t elem) {
+    const bool ext = a.rope.extension != 0;
+    const int hpm = a.heads_per_mask;
+    const int groups = (a.max_chunks + 31) / 32;
+    const int64_t wide_items = static_cast<int64_t>(a.n_masks) * groups * hpm;
+    if (!ext && a.scores_out == nullptr && a.chunk_size > 8 && hpm <= 8 &&
+        align_up(static_cast<size_t>(a.n_masks) * 4, 256) + static_cast<size_t>(a.n_masks) * hpm * a.max_chunks * 4 <=
+            a.workspace_bytes &&
+        wide_items > 2048)
+        return HP_STAGE_WIDE;
+    if (!ext && a.chunk_size <= 8 && 32 % a.chunk_size == 0 && (a.n_q_heads / a.keys.n_kv) % hpm == 0)
+        return HP_STAGE_ALLROWS;
+    if (!ext && elem == 2 && kLookahead) return HP_STAGE_LOOKAHEAD;
+    return HP_STAGE_CLASSIC;
+}
+
 template <typename T, bool EXT>
 cudaError_t launch_stage(const hp_decode_stage_args& a, float* scores, int* tickets, cudaStream_t s) {
     using G = RowGeom<T>;
@@ -1407,10 +1426,8 @@ cudaError_t launch_stage(const hp_decode_stage_args& a, float* scores, int* tick
     int head_planes = 1;
     const int groups = (a.max_chunks + 31) / 32;
     const int64_t wide_items = static_cast<int64_t>(a.n_masks) * groups * hpm;
-    if (!EXT && a.scores_out == nullptr && a.chunk_size > 8 && hpm <= 8 &&
-        align_up(static_cast<size_t>(a.n_masks) * 4, 256) + static_cast<size_t>(a.n_masks) * hpm * a.max_chunks * 4 <=
-            a.workspace_bytes &&
-        wide_items > 2048) {
+    const int variant = stage_variant(a, sizeof(T));
+    if (variant == HP_STAGE_WIDE) {
         // big stage: one wave of 7-warp CTAs, per-head scores (decode_stage_wide_kernel)
         const size_t smem3 = static_cast<size_t>(kWideWarps) * 32 * G::stride;
         auto k3 = decode_stage_wide_kernel<T>;
@@ -1419,7 +1436,7 @@ cudaError_t launch_stage(const hp_decode_stage_args& a, float* scores, int* tick
         head_planes = hpm;
         e = launch_pdl(k3, dim3(static_cast<unsigned>((wide_items + kWideWarps - 1) / kWideWarps)), dim3(kWideWarps * 32),
                        smem3, s, a, scores, groups);
-    } else if (!EXT && a.chunk_size <= 8 && 32 % a.chunk_size == 0 && (a.n_q_heads / a.keys.n_kv) % hpm == 0) {
+    } else if (variant == HP_STAGE_ALLROWS) {
         // short chunks: gather every row of a chunk at once (decode_stage_allrows_kernel)
         const size_t smem2 = static_cast<size_t>(kAllRowsWarps) * 32 * G::stride + static_cast<size_t>(hpm) * kD * 6;
         const int per_cta = kAllRowsWarps * (32 / a.chunk_size);
@@ -1428,7 +1445,7 @@ cudaError_t launch_stage(const hp_decode_stage_args& a, float* scores, int* tick
         if (e != cudaSuccess) return e;
         e = launch_pdl(k2, dim3((a.max_chunks + per_cta - 1) / per_cta, a.n_masks), dim3(kAllRowsWarps * 32), smem2, s,
                        a, scores);
-    } else if (!EXT && sizeof(T) == 2 && kLookahead) {
+    } else if (variant == HP_STAGE_LOOKAHEAD) {
         // latency-bound descents: two comparisons per gather round (decode_stage_look_kernel)
         const size_t smem4 = static_cast<size_t>(nw) * kLookSlots * 32 * G::stride + static_cast<size_t>(nw) * kD * 6 +
                              static_cast<size_t>(hpm) * 32 * cg * 4;
@@ -1478,7 +1495,8 @@ cudaError_t launch_bsa(const hp_decode_bsa_args& a, float* part, int* tickets, i
 // cluster variant: grid (splits, groups), cluster (splits, 1, 1), bf16 without RoPE
 constexpr int kBsaCluThreads = 512, kBsaCluMaxKeys = 256, kBsaMaxCluster = 16;
 template <int HC>
-cudaError_t launch_bsa_cluster(const hp_decode_bsa_args& a, int splits, int kpc, cudaStream_t s) {
+cudaError_t launch_bsa_cluster(const hp_decode_bsa_args& a, int splits, int kpc, cudaStream_t s,
+                               bool query_only = false) {
     using S = BsaSmem<bf16_t, HC, kBsaCluMaxKeys, kBsaCluThreads / 64>;
     auto kern = decode_bsa_kernel<bf16_t, HC, false, kBsaCluThreads, kBsaCluMaxKeys, true>;
     static int checked_splits[kBsaMaxCluster + 1] = {};  // max active clusters, -1 = none
@@ -1509,6 +1527,7 @@ cudaError_t launch_bsa_cluster(const hp_decode_bsa_args& a, int splits, int kpc,
     // every head group's cluster resident in one wave, else the ticket path is faster
     // (B200, 162 KB CTAs: 7 clusters of 11-16 fit, 15 of 7-9)
     if (checked_splits[splits] < static_cast<int>(cfg.gridDim.y)) return cudaErrorNotSupported;
+    if (query_only) return cudaSuccess;
     e = cudaLaunchKernelEx(&cfg, kern, a, static_cast<float*>(nullptr), static_cast<int*>(nullptr), splits, kpc);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
@@ -1572,7 +1591,12 @@ extern "C" int hp_decode_stage(const hp_decode_stage_args* ap, void* stream) {
                               a.max_chunks, kTopkMaxKeys);
     const size_t need = hp_decode_stage_workspace_bytes(a.n_masks, a.max_chunks);
     if (!a.workspace || a.workspace_bytes < need) return hph::set_error(HP_INVALID_ARGUMENT, "hp_decode_stage: workspace too small");
-    if (a.rope.extension) {
+    // identity stages (pruning.cpp:159-168) never rotate, so the reference never range-checks
+    // them: skip the check when the stage is provably the identity from host-known bounds
+    const int64_t kk = a.keep / a.chunk_size;
+    const bool identity = a.in_count ? a.max_chunks <= kk
+                                     : (a.in_count_const <= a.keep || (a.in_count_const + a.chunk_size - 1) / a.chunk_size <= kk);
+    if (a.rope.extension && !identity) {
         const int pol = a.rope.layer > a.rope.early_cutoff ? a.rope.late_policy : a.rope.early_policy;
         if (pol != HP_ROPE_CHUNK_INDEXED && pol != HP_ROPE_RELATIVE)
             return hph::set_error(HP_LOGIC_ERROR, "query_position: policy not applicable to pruning");
@@ -1629,7 +1653,45 @@ extern "C" size_t hp_decode_bsa_workspace_bytes(int32_t n_q_heads, int32_t max_s
     return align_up(static_cast<size_t>(n_q_heads) * splits * kBsaRec * 4, 256) + align_up(static_cast<size_t>(n_q_heads) * 4, 256);
 }
 
-extern "C" int hp_decode_bsa(const hp_decode_bsa_args* ap, void* stream) {
+// one cluster per head group when the selection fits 16 CTAs of <= 256 keys and every
+// group's cluster is co-resident; false = the ticket-merge kernel
+static bool try_bsa_cluster(const hp_decode_bsa_args& a, int64_t max_sel, int hc, cudaStream_t s, bool query_only) {
+    if (a.kv.dtype != HP_BF16 || a.rope.extension || !kBsaUseCluster) return false;
+    const int64_t kc = std::max<int64_t>(kBsaMaxKeys, ((max_sel + kBsaMaxCluster - 1) / kBsaMaxCluster + 15) / 16 * 16);
+    const int sc = static_cast<int>((max_sel + kc - 1) / kc);
+    if (!(kc <= kBsaCluMaxKeys && sc >= 2 && sc <= kBsaMaxCluster)) return false;
+    cudaError_t e;
+    switch (hc) {
+        case 1: e = launch_bsa_cluster<1>(a, sc, static_cast<int>(kc), s, query_only); break;
+        case 2: e = launch_bsa_cluster<2>(a, sc, static_cast<int>(kc), s, query_only); break;
+        case 4: e = launch_bsa_cluster<4>(a, sc, static_cast<int>(kc), s, query_only); break;
+        default: e = launch_bsa_cluster<8>(a, sc, static_cast<int>(kc), s, query_only); break;
+    }
+    if (e == cudaSuccess) return true;
+    cudaGetLastError();  // not resident-able here: the ticket path
+    return false;
+}
+
+static int decode_bsa_impl(const hp_decode_bsa_args* ap, void* stream, int* variant_out);
+
+extern "C" int hp_decode_bsa(const hp_decode_bsa_args* ap, void* stream) { return decode_bsa_impl(ap, stream, nullptr); }
+
+extern "C" int hp_decode_bsa_variant(const hp_decode_bsa_args* ap, int32_t* variant) {
+    if (!variant) return hph::set_error(HP_INVALID_ARGUMENT, "hp_decode_bsa_variant: null output");
+    int v = -1;
+    const int rc = decode_bsa_impl(ap, nullptr, &v);
+    *variant = v;
+    return rc;
+}
+
+extern "C" int hp_decode_stage_variant(const hp_decode_stage_args* ap, int32_t* variant) {
+    if (!ap || !variant) return hph::set_error(HP_INVALID_ARGUMENT, "hp_decode_stage_variant: null pointer");
+    *variant = stage_variant(*ap, ap->keys.dtype == HP_BF16 ? 2 : 4);
+    return HP_OK;
+}
+
+static int decode_bsa_impl(const hp_decode_bsa_args* ap, void* stream, int* variant_out) {
+    const bool query_only = variant_out != nullptr;
     if (!ap) return hph::set_error(HP_INVALID_ARGUMENT, "hp_decode_bsa: null args");
     const hp_decode_bsa_args& a = *ap;
     if (a.kv.d != kD) return hph::set_error(HP_INVALID_ARGUMENT, "hp_decode_bsa: fused decode path needs head_dim 128");
@@ -1639,13 +1701,14 @@ extern "C" int hp_decode_bsa(const hp_decode_bsa_args* ap, void* stream) {
     const int64_t pos = a.query_position;
     const int64_t sink_end = std::min<int64_t>(a.sink_tokens, pos + 1);
     const int64_t stream_begin = std::max<int64_t>(pos + 1 > a.stream_tokens ? pos + 1 - a.stream_tokens : 0, sink_end);
-    const int64_t max_sel = sink_end + a.max_mask + (pos + 1 - stream_begin);
+    // the selected set is a subset of [0, pos]: it never holds more than pos + 1 tokens,
+    // so the grid is sized by the tighter of the two bounds (the reference's
+    // streaming_positions check, sparse_attention.cpp:43-50, can then never fire)
+    const int64_t max_sel = std::min<int64_t>(sink_end + a.max_mask + (pos + 1 - stream_begin), pos + 1);
     if (max_sel <= 0) return hph::set_error(HP_INVALID_ARGUMENT, "attention_row: empty selected set");
-    if (a.rope.extension) {
-        if (pos >= a.rope.rope_max) return hph::set_error(HP_OUT_OF_RANGE, "apply_rope: position %lld >= max_position %lld",
-                                                          static_cast<long long>(pos), static_cast<long long>(a.rope.rope_max));
-        if (max_sel > pos + 1) return hph::set_error(HP_LOGIC_ERROR, "streaming_positions: selected tokens cannot fit below position");
-    }
+    if (a.rope.extension && pos >= a.rope.rope_max)
+        return hph::set_error(HP_OUT_OF_RANGE, "apply_rope: position %lld >= max_position %lld",
+                              static_cast<long long>(pos), static_cast<long long>(a.rope.rope_max));
     const int hc = bsa_hc(a.n_q_heads, a.kv.n_kv, a.heads_per_mask);
     const int kpc = bsa_keys_per_cta(max_sel, a.n_q_heads / hc);
     const int splits = static_cast<int>((max_sel + kpc - 1) / kpc);
@@ -1657,20 +1720,13 @@ extern "C" int hp_decode_bsa(const hp_decode_bsa_args* ap, void* stream) {
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const bool ext = a.rope.extension != 0;
     cudaError_t e;
-    if (a.kv.dtype == HP_BF16 && !ext && kBsaUseCluster) {
-        // one cluster per head group when the selection fits 16 CTAs of <= 256 keys
-        const int64_t kc = std::max<int64_t>(kBsaMaxKeys, ((max_sel + kBsaMaxCluster - 1) / kBsaMaxCluster + 15) / 16 * 16);
-        const int sc = static_cast<int>((max_sel + kc - 1) / kc);
-        if (kc <= kBsaCluMaxKeys && sc >= 2 && sc <= kBsaMaxCluster) {
-            switch (hc) {
-                case 1: e = launch_bsa_cluster<1>(a, sc, static_cast<int>(kc), s); break;
-                case 2: e = launch_bsa_cluster<2>(a, sc, static_cast<int>(kc), s); break;
-                case 4: e = launch_bsa_cluster<4>(a, sc, static_cast<int>(kc), s); break;
-                default: e = launch_bsa_cluster<8>(a, sc, static_cast<int>(kc), s); break;
-            }
-            if (e == cudaSuccess) return HP_OK;
-            cudaGetLastError();  // not resident-able here: the ticket path below
-        }
+    if (try_bsa_cluster(a, max_sel, hc, s, query_only)) {
+        if (query_only) *variant_out = HP_BSA_CLUSTER;
+        return HP_OK;
+    }
+    if (query_only) {
+        *variant_out = HP_BSA_TICKET;
+        return HP_OK;
     }
     if (a.kv.dtype == HP_BF16) e = ext ? dispatch_bsa_hc<bf16_t, true>(a, hc, part, tickets, splits, kpc, s) : dispatch_bsa_hc<bf16_t, false>(a, hc, part, tickets, splits, kpc, s);
     else e = ext ? dispatch_bsa_hc<float, true>(a, hc, part, tickets, splits, kpc, s) : dispatch_bsa_hc<float, false>(a, hc, part, tickets, splits, kpc, s);

@@ -246,6 +246,9 @@ __global__ void __launch_bounds__(kThreads, 1) bsa_prefill_tc_kernel(const hp_bs
     const bool my_ok = my_r < rows_here;
     const int64_t my_pos = pos_first + (my_ok ? my_r : rows_here - 1);
     const int64_t my_sb = stream_begin(my_pos);
+    // the block's first row is past every sink of the union (a block overlapping the sink
+    // region, e.g. a prompt prefilled from position 0, keeps the causal test per entry)
+    const bool all_see_low = pos_first + 1 >= s0;
     // softmax in base 2: scores scaled by log2(e)/sqrt(d), exponentials on MUFU.EX2
     const float scale = 1.4426950408889634f / sqrtf(static_cast<float>(kHD));
     float run_m = -INFINITY, run_l = 0.f;  // run_l: this thread's half of the row sum
@@ -334,9 +337,10 @@ __global__ void __launch_bounds__(kThreads, 1) bsa_prefill_tc_kernel(const hp_bs
         const int ub = tile * kTN + half * 64;
         const int32_t pos32 = my_ok ? static_cast<int32_t>(my_pos) : -1;
         const int32_t sb32 = static_cast<int32_t>(my_sb), sink32 = static_cast<int32_t>(min64(sink, 0x7fffffff));
-        if (my_ok && ub + kTN / 2 <= s0 + nmid) {
+        if (my_ok && all_see_low && ub + kTN / 2 <= s0 + nmid) {
             // sinks and mask entries (union index < s0 + nmid) precede every row of the
-            // block (< stream_begin(first row)): all selected, no per-entry test
+            // block (< stream_begin(first row), and the first row already sees every
+            // sink): all selected, no per-entry test
 #pragma unroll
             for (int jj = 0; jj < kTN / 2; ++jj) tm4[jj & 3] = fmaxf(tm4[jj & 3], sv[jj]);
         } else {

@@ -485,6 +485,24 @@ class FusedDecodeLayer:
         self.ws_bsa = torch.zeros(lib().hp_decode_bsa_workspace_bytes(n_q_heads, max_sel),
                                   dtype=torch.uint8, device=dev)
         self._keep = []  # ctypes objects alive across async launches
+        self._last_args = [None] * (S + 1)  # per stage + BSA: the last launch's arguments
+
+    def dispatch(self) -> list[str]:
+        """Which kernel each stage of the last run() launched, then the BSA's
+        (hp_decode_stage_variant / hp_decode_bsa_variant); None = not run."""
+        out = []
+        for i, a in enumerate(self._last_args):
+            if a is None:
+                out.append(None)
+                continue
+            v = C.c_int32(-1)
+            if i < len(self.stages):
+                check(lib().hp_decode_stage_variant(C.byref(a), C.byref(v)))
+                out.append(_capi.STAGE_VARIANTS[v.value])
+            else:
+                check(lib().hp_decode_bsa_variant(C.byref(a), C.byref(v)))
+                out.append(_capi.BSA_VARIANTS[v.value])
+        return out
 
     def run(self, t: int, refresh=None, stream=None, materialize: bool = True,
             mat_stream: torch.cuda.Stream | None = None) -> torch.Tensor:
@@ -499,6 +517,15 @@ class FusedDecodeLayer:
         sp = C.c_void_p(_stream(stream))
         kvv = self.kv.view(t)
         chains = [None] * S
+        # per-stage bound on the input length at this context (stage i reads at most
+        # min(n0, k_{i-1}) tokens): tight grids, and provably-identity stages are known
+        # on the host (the reference never rotates — so never range-checks — those)
+        bound, prev = [], n0
+        for i, (_, lc, keep) in enumerate(self.stages):
+            if i > 0 and not refresh[i - 1]:
+                prev = self.stages[i - 1][2]  # a cached list from an earlier step: only k bounds it
+            bound.append(max(1, min(self.max_chunks[i], ceil_div(prev, lc))))
+            prev = min(prev, keep)
         for i, (_, lc, keep) in enumerate(self.stages):
             if i == 0:
                 in_ref, in_count, const = _ref_range(self.sink), None, n0
@@ -511,7 +538,7 @@ class FusedDecodeLayer:
                     chunk_size=lc, keep=keep, n_masks=self.n_masks, heads_per_mask=self.hpm,
                     n_q_heads=self.n_q_heads, stream_tokens=self.stream_tokens, q=_ptr(self.q),
                     query_position=pos, in_=in_ref, in_count=_ptr(in_count), in_count_const=const,
-                    max_chunks=self.max_chunks[i], sel_stride=self.sel[i].shape[-1],
+                    max_chunks=bound[i], sel_stride=self.sel[i].shape[-1],
                     sel_out=_ptr(self.sel[i]), out_count=_ptr(self.count[i]),
                     workspace=_ptr(self.ws_stage), workspace_bytes=self.ws_stage.numel(),
                     keys=kvv, rope=self.policy.ctx(self.layer1, self.rope),
@@ -520,6 +547,7 @@ class FusedDecodeLayer:
                     list_out=_ptr(self.cache[i]) if i == S - 1 else None,
                     list_out_stride=self.cache[i].shape[-1])
                 check(lib().hp_decode_stage(C.byref(a), sp))
+                self._last_args[i] = a
                 chains[i] = (_ref_list(self.cache[i]) if i == S - 1
                              else _ref_push(in_ref, self.sel[i], lc))
             else:
@@ -534,6 +562,7 @@ class FusedDecodeLayer:
             # the last stage's cache is untouched this step: gather in the PDL prologue
             mask_stable=0 if refresh[-1] else 1)
         check(lib().hp_decode_bsa(C.byref(b), sp))
+        self._last_args[S] = b
         if materialize:
             idx = [i for i in range(S - 1) if refresh[i]]  # the last stage wrote its own
             if idx:

@@ -3,7 +3,7 @@
 Index work (stage outputs, masks) must be bit-exact; attention outputs within
 1e-3 relative (north_star's fp32 tolerance; bf16 configs feed both sides the
 same bf16-rounded values, so the same bound applies). Sizes are chosen so the
-oracle finishes in seconds; full-size properties live in test_gpu_fullsize.py.
+oracle finishes in seconds; the benchmarked full-size shapes are in test_gpu_headline.py.
 """
 from __future__ import annotations
 
@@ -370,24 +370,27 @@ def test_fused_step_host_matches_device_path():
             assert torch.equal(host.mask(i)[1], ref.mask(i)[1])
 
 
+@pytest.mark.parametrize("ext", [False, True])
 @pytest.mark.parametrize("t", [1, 7, 300, 1281, 1300, 2049, 5000, 40001])
-def test_fused_decode_short_and_ragged_contexts(port, t):
+def test_fused_decode_short_and_ragged_contexts(port, t, ext):
     """Edge contexts on the fused path (3k preset): shorter than the sinks, shorter than
     sink + stream (empty middle), a middle shorter than one stage-1 chunk, ragged last
-    pages and chunks — masks exact, outputs within 1e-3 of the oracle's decode body."""
+    pages and chunks — masks exact, outputs within 1e-3 of the oracle's decode body.
+    With RoPE extension too (short contexts must not be refused)."""
     D = _dev()
     dev = torch.device("cuda")
     stages = [(64, 256, 32768), (64, 32, 8192), (64, 8, 2048)]
     groups, hpm = 2, 4
     q, k, v = workload(17 + t, groups * hpm, groups, 1, t, 128, bf16=True)
     kv = D.PagedKV(torch.from_numpy(k), torch.from_numpy(v), page_size=64, dtype=torch.bfloat16)
+    rope = D.RopeTable(t + 2, 128) if ext else None
     layer = D.FusedDecodeLayer(kv, stages, sink=256, stream_tokens=1024, n_q_heads=groups * hpm,
-                               n_masks=groups)
+                               n_masks=groups, policy=D.RopePolicy(extension=ext), rope=rope)
     layer.q.copy_(torch.from_numpy(q[:, 0]).to(dev))
     out = layer.run(t).clone()
     torch.cuda.synchronize()
     masks, want_out, _ = port.decode_layer_step(q.reshape(groups, hpm, 128), k, v, stages, sink=256,
-                                                stream=1024, ext=False, layer1=4)
+                                                stream=1024, ext=ext, layer1=4)
     cl, cc = layer.mask()
     for g in range(groups):
         assert np.array_equal(cl[g, : int(cc[g])].cpu().numpy(), masks[g]), g
