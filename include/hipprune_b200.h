@@ -321,6 +321,53 @@ int hp_decode_bsa(const hp_decode_bsa_args* args, void* stream);
 enum hp_bsa_variant { HP_BSA_TICKET = 0, HP_BSA_CLUSTER = 1 };
 int hp_decode_bsa_variant(const hp_decode_bsa_args* args, int32_t* variant);
 
+/* ------------------------------------------------------------------------ *
+ * The whole per-layer decode body in two launches (d = 128, bf16 K/V, RoPE
+ * extension off): stage 0's descent (hp_decode_stage's kernels, scores only),
+ * then ONE kernel per layer in which a thread-block cluster per KV group runs
+ * stage 0's selection, every later due stage (descent + exact top-K), and the
+ * block-sparse attention with its log-sum-exp combine — the selections and the
+ * merge exchange data through distributed shared memory, so nothing between the
+ * stages is a kernel boundary. Same results as hp_decode_stage + hp_decode_bsa
+ * (selections index-exact; output within the fp32 tolerance).
+ * Replaces DecodeEngine::step's per-layer body (decode.cpp:225-273): stages due
+ * this step (refresh[i]) chain through each other (stage i reads stage i-1's list
+ * when i-1 also ran, else the cached list cache[i-1] with count[i-1]); the BSA
+ * reads the last stage's list. Stage i's kept chunk ids land in sel[i] and its
+ * output length in count[i] (the stage caches are then expanded on demand with
+ * hp_decode_materialize, e.g. on a side stream).
+ * ------------------------------------------------------------------------ */
+typedef struct hp_decode_layer_args {
+    int32_t n_stages;            /* 1..4                                                  */
+    int32_t chunk_size[4];
+    int32_t keep[4];
+    int32_t refresh[4];          /* 1 = stage due this step (refresh_due, decode.cpp:212-224) */
+    int32_t n_masks;             /* KV groups, one pooled mask each                       */
+    int32_t heads_per_mask;      /* 1, 2, 4 or 8; a mask's heads share one kv head        */
+    int32_t n_q_heads;
+    int32_t sink_tokens;
+    int32_t stream_tokens;
+    int32_t pad_;
+    const float* q;              /* [n_q_heads][128] fp32                                 */
+    int64_t query_position;      /* T - 1; stage 0 reads [n_sink, T - n_stream)           */
+    int32_t* sel[4];             /* [n_masks][sel_stride[i]] kept chunk ids (written if due) */
+    int32_t sel_stride[4];       /* >= keep[i] / chunk_size[i]                            */
+    int32_t* count[4];           /* [n_masks] stage output lengths (written if due)       */
+    const int32_t* cache[4];     /* [n_masks][cache_stride[i]] materialized stage lists   */
+    int64_t cache_stride[4];
+    float* out;                  /* [n_q_heads][128] fp32                                 */
+    void* workspace;             /* >= hp_decode_layer_workspace_bytes()                  */
+    size_t workspace_bytes;
+    hp_kv_view kv;               /* bf16, d = 128                                         */
+    const int32_t* keys_exact;   /* as in hp_decode_stage_args                            */
+} hp_decode_layer_args;
+
+size_t hp_decode_layer_workspace_bytes(int32_t n_masks, int32_t max_chunks0);
+/* 1 when hp_decode_layer takes this configuration, 0 otherwise (then use the
+ * per-stage entry points); no launch. */
+int hp_decode_layer_supported(const hp_decode_layer_args* args);
+int hp_decode_layer(const hp_decode_layer_args* args, void* stream);
+
 /* Append one token's K/V rows (DecodeEngine::step, decode.cpp:202-208): rows
  * [n_kv][d] (same dtype as the pools) land at `token` of the paged pools; keys_exact
  * (optional device int) is cleared if a new key breaks the exact-product range. */

@@ -103,6 +103,17 @@ class DecodeBsaArgs(C.Structure):
                 ("mask_stable", C.c_int32)]
 
 
+class DecodeLayerArgs(C.Structure):
+    _fields_ = [("n_stages", C.c_int32), ("chunk_size", C.c_int32 * 4), ("keep", C.c_int32 * 4),
+                ("refresh", C.c_int32 * 4), ("n_masks", C.c_int32), ("heads_per_mask", C.c_int32),
+                ("n_q_heads", C.c_int32), ("sink_tokens", C.c_int32), ("stream_tokens", C.c_int32),
+                ("pad_", C.c_int32), ("q", C.c_void_p), ("query_position", C.c_int64),
+                ("sel", C.c_void_p * 4), ("sel_stride", C.c_int32 * 4), ("count", C.c_void_p * 4),
+                ("cache", C.c_void_p * 4), ("cache_stride", C.c_int64 * 4), ("out", C.c_void_p),
+                ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t), ("kv", KvView),
+                ("keys_exact", C.c_void_p)]
+
+
 class BsaPrefillArgs(C.Structure):
     _fields_ = [("n_q_heads", C.c_int32), ("heads_per_mask", C.c_int32), ("n_rows", C.c_int32),
                 ("block_size", C.c_int32), ("q", C.c_void_p), ("query_offset", C.c_int64),
@@ -126,7 +137,8 @@ EXPORTS = ["hp_last_error", "hp_version", "hp_device_available", "hp_build_rope_
            "hp_stage_workspace_bytes", "hp_prune_stage", "hp_remap_blocks",
            "hp_selected_indices", "hp_bsa_workspace_bytes", "hp_bsa", "hp_lse_merge",
            "hp_decode_stage_workspace_bytes", "hp_decode_stage", "hp_decode_bsa_workspace_bytes",
-           "hp_decode_bsa", "hp_decode_stage_variant", "hp_decode_bsa_variant", "hp_decode_materialize", "hp_decode_append", "hp_trace_enable", "hp_debug_cut",
+           "hp_decode_bsa", "hp_decode_stage_variant", "hp_decode_bsa_variant",
+           "hp_decode_layer_workspace_bytes", "hp_decode_layer_supported", "hp_decode_layer", "hp_decode_materialize", "hp_decode_append", "hp_trace_enable", "hp_debug_cut",
            "hp_cache_workspace_bytes", "hp_cache_commit", "hp_select_topk",
            "hp_bsa_prefill_smem_bytes", "hp_bsa_prefill", "hp_debug_prefill_progress"]
 
@@ -173,6 +185,14 @@ def lib():
     L.hp_decode_stage_variant.argtypes = [C.POINTER(DecodeStageArgs), C.POINTER(C.c_int32)]
     L.hp_decode_bsa_variant.restype = C.c_int
     L.hp_decode_bsa_variant.argtypes = [C.POINTER(DecodeBsaArgs), C.POINTER(C.c_int32)]
+    L.hp_decode_layer_workspace_bytes.restype = C.c_size_t
+    L.hp_decode_layer_workspace_bytes.argtypes = [C.c_int32, C.c_int32]
+    L.hp_decode_layer_supported.restype = C.c_int
+    L.hp_decode_layer_supported.argtypes = [C.POINTER(DecodeLayerArgs)]
+    L.hp_decode_layer.restype = C.c_int
+    L.hp_decode_layer.argtypes = [C.POINTER(DecodeLayerArgs), C.c_void_p]
+    L.hp_decode_layer_cluster.restype = C.c_int
+    L.hp_decode_layer_cluster.argtypes = [C.c_int]
     L.hp_decode_materialize.restype = C.c_int
     L.hp_decode_materialize.argtypes = [C.POINTER(ListRef), C.POINTER(C.c_void_p),
                                         C.POINTER(C.c_void_p), C.POINTER(C.c_int64), C.c_int32,

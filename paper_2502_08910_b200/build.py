@@ -18,7 +18,7 @@ LIB = PKG / "_lib"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",
               f"-I{ROOT / 'include'}", f"-I{CSRC}"]
-CUDA_SOURCES = ["prune.cu", "bsa.cu", "decode.cu", "cache.cu", "prefill.cu", "capi.cu"]
+CUDA_SOURCES = ["prune.cu", "bsa.cu", "decode.cu", "layer.cu", "cache.cu", "prefill.cu", "capi.cu"]
 
 
 def nvcc() -> str:

@@ -479,21 +479,58 @@ class FusedDecodeLayer:
         for (_, lc, keep) in self.stages:
             self.max_chunks.append(max(1, ceil_div(prev, lc)))
             prev = keep
-        ws_stage = max(lib().hp_decode_stage_workspace_bytes(n_masks, mc) for mc in self.max_chunks)
+        ws_stage = max(max(lib().hp_decode_stage_workspace_bytes(n_masks, mc) for mc in self.max_chunks),
+                       lib().hp_decode_layer_workspace_bytes(n_masks, self.max_chunks[0]))
         self.ws_stage = torch.zeros(ws_stage, dtype=torch.uint8, device=dev)
         max_sel = sink + self.stages[-1][2] + stream_tokens + 1
         self.ws_bsa = torch.zeros(lib().hp_decode_bsa_workspace_bytes(n_q_heads, max_sel),
                                   dtype=torch.uint8, device=dev)
         self._keep = []  # ctypes objects alive across async launches
         self._last_args = [None] * (S + 1)  # per stage + BSA: the last launch's arguments
+        self._fused = None  # hp_decode_layer (one cluster kernel after stage 0) when supported
+
+    def _run_fused(self, t, refresh, stream, materialize, mat_stream):
+        """The layer on hp_decode_layer: stage 0's descent + one cluster kernel; then the
+        refreshed stage caches are expanded (materialize) from the kept chunk ids."""
+        S = len(self.stages)
+        sp = C.c_void_p(_stream(stream))
+        a = self._layer_args(t, refresh)
+        check(lib().hp_decode_layer(C.byref(a), sp))
+        self._last_args = [self._stage0_args(t) if refresh[0] else None] + ["layer"] * S
+        if materialize:
+            chains = [None] * S
+            for i, (_, lc, keep) in enumerate(self.stages):
+                if i == 0:
+                    base = _ref_range(self.sink)
+                elif refresh[i - 1]:
+                    base = chains[i - 1]
+                else:
+                    base = _ref_list(self.cache[i - 1])
+                chains[i] = _ref_push(base, self.sel[i], lc) if refresh[i] else None
+            idx = [i for i in range(S) if refresh[i]]
+            if idx:
+                n = len(idx)
+                refs = (_capi.ListRef * n)(*[chains[i] for i in idx])
+                counts = (C.c_void_p * n)(*[_ptr(self.count[i]) for i in idx])
+                outs = (C.c_void_p * n)(*[_ptr(self.cache[i]) for i in idx])
+                strides = (C.c_int64 * n)(*[self.cache[i].shape[-1] for i in idx])
+                msp = sp
+                if mat_stream is not None:
+                    ev = torch.cuda.Event()
+                    ev.record(stream if stream is not None else torch.cuda.current_stream())
+                    mat_stream.wait_event(ev)
+                    msp = C.c_void_p(mat_stream.cuda_stream)
+                check(lib().hp_decode_materialize(refs, counts, outs, strides, n, self.n_masks,
+                                                  max(self.stages[i][2] for i in idx), msp))
+        return self.out
 
     def dispatch(self) -> list[str]:
         """Which kernel each stage of the last run() launched, then the BSA's
         (hp_decode_stage_variant / hp_decode_bsa_variant); None = not run."""
         out = []
         for i, a in enumerate(self._last_args):
-            if a is None:
-                out.append(None)
+            if a is None or isinstance(a, str):
+                out.append(a)
                 continue
             v = C.c_int32(-1)
             if i < len(self.stages):
@@ -504,6 +541,31 @@ class FusedDecodeLayer:
                 out.append(_capi.BSA_VARIANTS[v.value])
         return out
 
+    def _layer_args(self, t: int, refresh) -> "_capi.DecodeLayerArgs":
+        S = len(self.stages)
+        a = _capi.DecodeLayerArgs()
+        a.n_stages = S
+        for i, (_, lc, keep) in enumerate(self.stages):
+            a.chunk_size[i], a.keep[i], a.refresh[i] = lc, keep, int(bool(refresh[i]))
+            a.sel[i], a.sel_stride[i] = _ptr(self.sel[i]), self.sel[i].shape[-1]
+            a.count[i] = _ptr(self.count[i])
+            a.cache[i], a.cache_stride[i] = _ptr(self.cache[i]), self.cache[i].shape[-1]
+        a.n_masks, a.heads_per_mask, a.n_q_heads = self.n_masks, self.hpm, self.n_q_heads
+        a.sink_tokens, a.stream_tokens = self.sink, self.stream_tokens
+        a.q, a.query_position, a.out = _ptr(self.q), t - 1, _ptr(self.out)
+        a.workspace, a.workspace_bytes = _ptr(self.ws_stage), self.ws_stage.numel()
+        a.kv = self.kv.view(t)
+        a.keys_exact = _ptr(self.kv.keys_exact)
+        return a
+
+    def fused_supported(self) -> bool:
+        """hp_decode_layer takes this configuration (bf16, d = 128, RoPE extension off,
+        1/2/4/8 heads per KV group, <= 4 stages) and it was not disabled (HP_LAYER=0)."""
+        import os
+        if os.environ.get("HP_LAYER", "1") == "0" or self.policy.extension or len(self.stages) > 4:
+            return False
+        return bool(lib().hp_decode_layer_supported(C.byref(self._layer_args(self.kv.t_kv, [True] * len(self.stages)))))
+
     def run(self, t: int, refresh=None, stream=None, materialize: bool = True,
             mat_stream: torch.cuda.Stream | None = None) -> torch.Tensor:
         """One layer step at context length t. ``mat_stream``: materialize the refreshed
@@ -511,6 +573,13 @@ class FusedDecodeLayer:
         caches are next read) so the copy is off the layer's critical path."""
         S = len(self.stages)
         refresh = list(refresh) if refresh is not None else [True] * S
+        if self._fused is None:
+            self._fused = self.fused_supported()
+        # hp_decode_layer when a stage with a successor stage is due (its selection and the
+        # next stage chain inside one kernel); steps that only rescore the last stage or reuse
+        # every cache run the per-stage kernels, measured faster there (DESIGN.md §5)
+        if self._fused and (self._fused == "always" or any(refresh[:-1])):
+            return self._run_fused(t, refresh, stream, materialize, mat_stream)
         pos = t - 1
         upper = t - self.stream_tokens if t > self.stream_tokens else 0
         n0 = max(0, upper - self.sink)
@@ -580,6 +649,19 @@ class FusedDecodeLayer:
                 check(lib().hp_decode_materialize(refs, counts, outs, strides, n, self.n_masks,
                                                   max(self.stages[i][2] for i in idx), msp))
         return self.out
+
+    def _stage0_args(self, t: int):
+        """Stage 0's descent arguments as hp_decode_layer builds them (dispatch query)."""
+        (_, lc, keep) = self.stages[0]
+        upper = t - self.stream_tokens if t > self.stream_tokens else 0
+        n0 = max(0, upper - self.sink)
+        return _capi.DecodeStageArgs(
+            chunk_size=lc, keep=keep, n_masks=self.n_masks, heads_per_mask=self.hpm,
+            n_q_heads=self.n_q_heads, stream_tokens=self.stream_tokens, q=_ptr(self.q),
+            query_position=t - 1, in_=_ref_range(self.sink), in_count=None, in_count_const=n0,
+            max_chunks=max(1, ceil_div(n0, lc)), sel_stride=self.sel[0].shape[-1], sel_out=None,
+            out_count=_ptr(self.count[0]), workspace=_ptr(self.ws_stage),
+            workspace_bytes=self.ws_stage.numel(), keys=self.kv.view(t), keys_exact=_ptr(self.kv.keys_exact))
 
     def run_stage(self, t: int, i: int = 0, stream=None, select: bool = True) -> None:
         """Launch only stage i (descent, + selection unless select=False) on its input:

@@ -32,13 +32,16 @@ SINK, STREAM = 256, 1024
 GROUPS, HPM, D = 8, 4, 128
 
 
-def _run(t, seed, refresh=None):
+def _run(t, seed, fused=True):
     from paper_2502_08910_b200 import device as Dv, synth
     Dv.require_cuda()
     q, k, v = synth.generate(GROUPS * HPM, GROUPS, t, D, seed=seed)
     kv = Dv.PagedKV(k, v, page_size=64, dtype=torch.bfloat16)
     layer = Dv.FusedDecodeLayer(kv, STAGES, sink=SINK, stream_tokens=STREAM, n_q_heads=GROUPS * HPM,
                                 n_masks=GROUPS)
+    # "always": every refresh pattern on hp_decode_layer (the default takes the per-stage
+    # kernels for steps that refresh no stage with a successor); False: per-stage kernels only
+    layer._fused = "always" if fused else False
     layer.q.copy_(q[:, 0])
     out = layer.run(t).clone()
     torch.cuda.synchronize()
@@ -66,24 +69,36 @@ def _check_groups(port, t, q, k, v, layer, out):
         del kg, vg
 
 
-def test_headline_c3_1m_8groups_exact(port):
-    """The bench's full-refresh step at T = 2^20, all 8 KV groups: wide stage-1 kernel +
-    ticket-merge BSA, every stage list and mask index-exact, outputs within 1e-3."""
+@pytest.mark.parametrize("path", ["layer", "per_stage"])
+def test_headline_c3_1m_8groups_exact(port, path):
+    """The bench's full-refresh step at T = 2^20, all 8 KV groups, on the path the bench
+    times (hp_decode_layer: the one-wave stage-1 kernel + one cluster kernel per layer)
+    and on the per-stage kernels (wide stage 1 + ticket-merge BSA): every stage list and
+    mask index-exact, outputs within 1e-3."""
     t = 1 << 20
-    q, k, v, layer, out = _run(t, seed=1)
+    q, k, v, layer, out = _run(t, seed=1, fused=path == "layer")
     kinds = layer.dispatch()
     assert kinds[0] == "wide", kinds
-    assert kinds[-1] == "ticket", kinds
+    if path == "layer":
+        assert layer._fused and kinds[1:] == ["layer"] * 3, kinds
+    else:
+        assert kinds[-1] == "ticket", kinds
     _check_groups(port, t, q, k, v, layer, out)
-    # the amortized schedule's BSA-only step reuses the cached mask (PDL-prologue gathers)
+    # the amortized schedule's BSA-only step reuses the cached mask: same kernel, same output
     out2 = layer.run(t, refresh=[False] * 3).clone()
     torch.cuda.synchronize()
     assert torch.equal(out2, out)
+    if path == "layer":  # the default (hybrid) dispatch's BSA-only step: the per-stage BSA kernel
+        layer._fused = True
+        out3 = layer.run(t, refresh=[False] * 3).clone()
+        torch.cuda.synchronize()
+        assert ((out3 - out).abs().max() / out.abs().max()).item() <= 1e-5
 
 
-def test_c2_128k_8groups_exact(port):
+@pytest.mark.parametrize("path", ["layer", "per_stage"])
+def test_c2_128k_8groups_exact(port, path):
     """C2: T = 128K, all 8 KV groups, bf16 — every stage list and mask exact."""
     t = 1 << 17
-    q, k, v, layer, out = _run(t, seed=2)
+    q, k, v, layer, out = _run(t, seed=2, fused=path == "layer")
     assert all(x is not None for x in layer.dispatch())
     _check_groups(port, t, q, k, v, layer, out)

@@ -293,10 +293,11 @@ def test_fused_decode_layer_step(port, case):
             assert np.array_equal(got, masks[g]), g
         assert_close(out.cpu().numpy().reshape(groups, hpm, 128), want_out)
     # a step that reuses every cache gathers in the BSA's PDL prologue (mask_stable):
-    # same mask, same output
+    # same mask, same output (the refresh step may have run on hp_decode_layer, whose
+    # split-K partition differs: equal up to fp32 summation order)
     out2 = layer.run(t, refresh=[False] * 3).clone()
     torch.cuda.synchronize()
-    assert torch.equal(out2, out)
+    assert ((out2 - out).abs().max() / out.abs().max()).item() <= 1e-5
 
 
 def test_fused_decode_refresh_schedule():
