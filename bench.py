@@ -11,11 +11,14 @@ synthetic Q/K/V (reference generator recipe, torch RNG). The amortized
 (16,8,4) stage-cache schedule ("Total") and the BSA-only step are reported
 alongside.
 
-Multi-GPU (torchrun, one process per GPU): weak scaling over independent
-(layer, KV-group) units (groups never exchange data) — every
-rank runs the full 8-group step on its own L = 8 layers (64 units per GPU), no
-data-path collective. value = whole-job µs per layer = (max-over-ranks step time)
-/ (L x N).
+Multi-GPU (torchrun, one process per GPU): KV-head-group sharding (SURVEY.md §8(e),
+C3; paper_2502_08910_b200/kvshard.py) — rank r of N owns KV groups
+[8r/N, 8(r+1)/N) of every layer and runs the whole per-layer body for them; groups
+never exchange data, so there is no data-path collective. Strong scaling: the layer
+step (all 8 groups) is fixed and split N ways; value = the layer's latency = the
+max over ranks of each rank's step time / L. The optional output all-gather
+(NCCL, 16 KB per layer) is timed separately as `allgather_us`. The workload is
+generated per (layer, group) seed, so every N processes identical data.
 
 `--impl reference` times the reference's own CPU implementation of the same
 step (oracle/_ref, the unmodified reference library; the C port if it was not
@@ -54,6 +57,9 @@ def parse():
     p.add_argument("--layers", type=int, default=8,
                    help="layers per decode step (distinct KV each); value = step time / layers")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--shard-of", type=int, default=0,
+                   help="dev: run as rank 0 of an N-way KV-group split in ONE process (no process "
+                        "group) to measure one GPU's share of the N-GPU step")
     return p.parse_args()
 
 
@@ -65,11 +71,13 @@ def dist_env():
 
 
 def config(args, world):
+    gpr = GROUPS // max(1, world)
     return {"workload": f"C3 decode, T={args.ctx}, KV in HBM, full-refresh step over {args.layers} layers "
                         f"(distinct KV per layer), reported per layer",
             "context": args.ctx, "q_heads": GROUPS * HPM, "kv_heads": GROUPS, "head_dim": D,
             "preset": "3k", "stages": STAGES, "sink": SINK, "stream": STREAM,
-            "units_per_gpu": f"{GROUPS * args.layers} (layer, KV-group) units ({args.layers} layers x {GROUPS} groups)", "parallelism": f"kv-group x{world}",
+            "units_per_gpu": f"{gpr * args.layers} (layer, KV-group) units ({args.layers} layers x {gpr} groups)",
+            "parallelism": f"kv-group x{world} (rank r owns groups [{gpr}r, {gpr}(r+1)) of every layer)",
             "layers_per_step": args.layers,
             "l2": "flushed before every timed step: 512 MB write, then 512 MB read (dirty lines evicted)"}
 
@@ -137,16 +145,21 @@ def cpu_reference_step(q, k, v, threads):
     return secs, kind
 
 
-def host_workload(t, seed):
-    """The same synthetic Q/K/V as the GPU arm, as host fp32 (bf16-rounded)."""
+def host_workload(t, layer=0):
+    """The same synthetic Q/K/V as the GPU arm's layer `layer` (per (layer, group) seeds),
+    as host fp32 (bf16-rounded)."""
+    import numpy as np
     import torch
     from paper_2502_08910_b200 import synth
     dev = "cuda" if torch.cuda.is_available() else "cpu"
-    q, k, v = synth.generate(GROUPS * HPM, GROUPS, t, D, seed=seed, device=dev)
-    qh = q[:, 0].float().cpu().numpy().reshape(GROUPS, HPM, D)
-    kh = k.float().cpu().numpy()
-    vh = v.float().cpu().numpy()
-    return qh, kh, vh
+    qs, ks, vs = [], [], []
+    for g in range(GROUPS):
+        q, k, v = synth.generate(HPM, 1, t, D, seed=1 + 1000 * layer + g, device=dev)
+        qs.append(q[:, 0].float().cpu().numpy())
+        ks.append(k.float().cpu().numpy())
+        vs.append(v.float().cpu().numpy())
+        del q, k, v
+    return np.stack(qs), np.concatenate(ks), np.concatenate(vs)
 
 
 def run_reference(args, rank, world):
@@ -154,7 +167,7 @@ def run_reference(args, rank, world):
         return 0
     import numpy as np
     threads = min(GROUPS, os.cpu_count() or 1)
-    q, k, v = host_workload(args.ctx, 1)
+    q, k, v = host_workload(args.ctx, 0)
     times = []
     kind = None
     for i in range(args.warmup + args.steps):
@@ -182,7 +195,7 @@ def main():
         return run_reference(args, rank, world)
 
     import torch
-    from paper_2502_08910_b200 import device as D_, synth
+    from paper_2502_08910_b200 import device as D_, kvshard, synth
 
     # one GPU per rank; HP_BENCH_BACKEND=gloo + fewer GPUs than ranks is a dev check of the
     # multi-rank logic on a 1-GPU box (ranks then share a device)
@@ -198,15 +211,30 @@ def main():
     t = args.ctx
     L = max(1, args.layers)
     n_q = max(16, args.steps + args.warmup)
+    split = args.shard_of if args.shard_of > 0 and world == 1 else world
+    g0, g1 = kvshard.group_range(GROUPS, split, rank)
+    ng = g1 - g0
     kvs, layers, qss = [], [], []
     for li in range(L):
-        q, k, v = synth.generate(GROUPS * HPM, GROUPS, t, D, t_q=n_q, seed=1 + rank * 1000 + li, device=dev)
-        kv = D_.PagedKV(k, v, page_size=64, dtype=torch.bfloat16, device=dev)
+        # this rank's KV groups of layer li, each from its own (layer, group) seed
+        parts = [synth.generate(HPM, 1, t, D, seed=1 + 1000 * li + g, device=dev) for g in range(g0, g1)]
+        # step 0's query is the generator's (what --impl reference uses); later steps draw
+        # fresh ones, per (layer, group) seed as well
+        def step_queries(q0, g):
+            gq = torch.Generator(device=dev)
+            gq.manual_seed(7 + 1000 * li + g)
+            more = torch.randn((HPM, n_q - 1, D), generator=gq, device=dev).to(torch.bfloat16).float()
+            return torch.cat([q0, more], 1)
+        q = torch.cat([step_queries(x[0], g) for x, g in zip(parts, range(g0, g1))])
+        k = torch.cat([x[1] for x in parts])
+        v = torch.cat([x[2] for x in parts])
+        del parts
+        shard = kvshard.KvGroupShardLayer(k, v, STAGES, sink=SINK, stream_tokens=STREAM, n_groups=GROUPS,
+                                          heads_per_group=HPM, world=split, rank=rank, device=dev)
         del k, v
-        kvs.append(kv)
-        layers.append(D_.FusedDecodeLayer(kv, STAGES, sink=SINK, stream_tokens=STREAM,
-                                          n_q_heads=GROUPS * HPM, n_masks=GROUPS, device=dev))
-        qss.append(q.transpose(0, 1).contiguous())  # [steps, heads, d]: a fresh query per step
+        kvs.append(shard.kv)
+        layers.append(shard.layer)
+        qss.append(q.transpose(0, 1).contiguous())  # [steps, own heads, d]: a fresh query per step
     kv, layer, qs = kvs[0], layers[0], qss[0]
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     flush_rd = torch.ones(512 << 20, dtype=torch.uint8, device=dev)
@@ -331,18 +359,36 @@ def main():
     achieved = alg_bytes / (s1_us * 1e-6) / 1e9
     traffic = None
     try:
+        if world > 1 or split > 1 or t != T_DEFAULT:
+            raise ValueError("the committed ncu capture is of the default N=1 configuration")
         prof = json.loads((ROOT / "profiles" / "stage1_ncu.json").read_text())
         traffic = prof.get("dram_bytes_per_launch")
     except Exception:
         pass
 
+    # ---- the optional output all-gather (every head on every rank), timed on its own
+    allgather_us = None
+    if world > 1:
+        for _ in range(3):
+            kvshard.gather_outputs(layers[0].out, world)
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(cur)
+        for ly in layers:
+            kvshard.gather_outputs(ly.out, world)
+        b.record(cur)
+        b.synchronize()
+        tt = torch.tensor([1000.0 * a.elapsed_time(b) / L], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        allgather_us = tt.item()
+
     # ---- e2e through the host-facing per-layer call, for every layer of the step:
     # pinned H2D (q + the new token's K/V) -> append -> layer step -> D2H of the output
-    h2d = GROUPS * HPM * D * 4 + 2 * GROUPS * D * 2
-    d2h = GROUPS * HPM * D * 4
+    h2d = ng * HPM * D * 4 + 2 * ng * D * 2
+    d2h = ng * HPM * D * 4
     q_host = [qq[: min(qq.shape[0], 8)].cpu().pin_memory() for qq in qss]
-    krow = torch.randn((GROUPS, D), device=dev).to(torch.bfloat16).cpu().pin_memory()
-    vrow = torch.randn((GROUPS, D), device=dev).to(torch.bfloat16).cpu().pin_memory()
+    krow = torch.randn((ng, D), device=dev).to(torch.bfloat16).cpu().pin_memory()
+    vrow = torch.randn((ng, D), device=dev).to(torch.bfloat16).cpu().pin_memory()
     e2e = []
     barrier()
     for i in range(args.warmup + args.steps):
@@ -381,24 +427,26 @@ def main():
             cpu = {"value": None, "unit": "us/layer", "cores": None, "kind": None, "sample": f"failed: {e}"}
 
     if rank == 0:
-        launches_per_step = (2 * len(STAGES) + 1 + 1) * L  # per layer: (descent + select) x 3, BSA, materialize
+        launches_per_step = 3 * L  # per layer: stage-1 descent, hp_decode_layer, cache materialize
         line = {
-            "metric": METRIC, "value": mean_step / world, "unit": "us/layer", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean_step / 1000.0,
-            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "metric": METRIC, "value": mean_step, "unit": "us/layer", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean_step * L / 1000.0,
+            "ms_per_step_note": f"one timed step = {L} layers",
+            "higher_is_better": False, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+            "dtype": "bf16",
             "data": "synthetic (reference generator recipe: N(0,1) Q/V, box-smoothed renormalised K; torch RNG)",
-            "config": config(args, world),
-            "full_refresh_us_per_gpu": mean_step, "amortized_us": amort_us / world,
+            "config": config(args, world) if split == world else dict(config(args, split), emulated=f"rank 0 of {split} in one process"),
+            "amortized_us": amort_us,
             "amortized_schedule": "refresh (16, 8, 4), averaged over whole cycles",
-            "bsa_only_us": bsa_us / world,
+            "bsa_only_us": bsa_us, "allgather_us": allgather_us,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "decode_stage_wide_kernel<bf16> (stage-1 descent, 8 KV groups)",
+                         "kernel": f"stage-1 descent ({layers[0].dispatch()[0] if layers[0].dispatch()[0] else 'stage 1'} kernel, {ng} KV groups)",
                          "kernel_us": s1_us, "algorithmic_bytes": alg_bytes,
                          "distinct_key_rows": rows, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"},
             "cpu_baseline": cpu,
-            "e2e": {"value": e2e_us / world, "unit": "us/layer", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h},
+            "e2e": {"value": e2e_us, "unit": "us/layer", "h2d_bytes_per_step": h2d * L,
+                    "d2h_bytes_per_step": d2h * L},
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk,
         }
