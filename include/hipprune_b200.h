@@ -286,6 +286,17 @@ int hp_select_topk(const float* scores, int64_t stride, int32_t n_masks, const i
                    int64_t n_in_const, int32_t chunk_size, int32_t keep, int32_t* sel_out,
                    int32_t sel_stride, int32_t* out_count, void* stream);
 
+/* Sequence-sharded stage selection (C5): `gathered` [n_ranks][n_masks][width] holds every
+ * rank's chunk scores of the stage (rank r's first counts[r][m] valid; ranks in global
+ * chunk order), as an all-gather leaves them. Per mask: the global stable top-K (same
+ * as hp_select_topk on the concatenated scores) -> sel_global / count_global, and this
+ * rank's part of it -> sel_local (kept chunk ids inside the rank's range, local, ascending)
+ * and len_local (the rank's share of the stage output). Identical on every rank. */
+int hp_select_topk_sharded(const float* gathered, const int32_t* counts, int32_t n_ranks, int32_t width,
+                           int32_t rank, int32_t n_masks, const int32_t* n_in, int64_t n_in_const,
+                           int32_t chunk_size, int32_t keep, int32_t* sel_global, int32_t sel_stride,
+                           int32_t* count_global, int32_t* sel_local, int32_t* len_local, void* stream);
+
 typedef struct hp_decode_bsa_args {
     int32_t n_q_heads;
     int32_t heads_per_mask;

@@ -139,7 +139,7 @@ EXPORTS = ["hp_last_error", "hp_version", "hp_device_available", "hp_build_rope_
            "hp_decode_stage_workspace_bytes", "hp_decode_stage", "hp_decode_bsa_workspace_bytes",
            "hp_decode_bsa", "hp_decode_stage_variant", "hp_decode_bsa_variant",
            "hp_decode_layer_workspace_bytes", "hp_decode_layer_supported", "hp_decode_layer", "hp_decode_materialize", "hp_decode_append", "hp_trace_enable", "hp_debug_cut",
-           "hp_cache_workspace_bytes", "hp_cache_commit", "hp_select_topk",
+           "hp_cache_workspace_bytes", "hp_cache_commit", "hp_select_topk", "hp_select_topk_sharded",
            "hp_bsa_prefill_smem_bytes", "hp_bsa_prefill", "hp_debug_prefill_progress"]
 
 
@@ -207,6 +207,10 @@ def lib():
     L.hp_select_topk.restype = C.c_int
     L.hp_select_topk.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_int64, C.c_int32,
                                  C.c_int32, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]
+    L.hp_select_topk_sharded.restype = C.c_int
+    L.hp_select_topk_sharded.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                         C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_void_p, C.c_int32,
+                                         C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
     L.hp_cache_workspace_bytes.restype = C.c_size_t
     L.hp_cache_workspace_bytes.argtypes = [C.c_int32, C.c_int32]
     L.hp_cache_commit.restype = C.c_int

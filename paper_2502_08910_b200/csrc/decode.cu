@@ -1465,6 +1465,97 @@ extern "C" int hp_select_topk(const float* scores, int64_t stride, int32_t n_mas
     return hph::check_cuda(e, "decode_topk_kernel");
 }
 
+// ------------------------------------------------------- sequence-sharded selection
+// C5: every rank all-gathered every rank's chunk scores of the stage ([R][M][W], rank r's
+// first counts[r][m] valid, ranks in global chunk order). One CTA per mask rebuilds the
+// global score vector in shared memory, runs the same exact top-K as the unsharded stage
+// (so every rank holds the same global selection), then cuts out this rank's part: the
+// kept chunks inside its range as local ids and its output length (the globally last
+// chunk may be short).
+constexpr int kShardMaxRanks = 64;
+__global__ void __launch_bounds__(kTopkThreads2)
+select_sharded_kernel(const float* gathered, const int32_t* counts, int R, int W, int rank, const int32_t* n_in,
+                      int64_t n_in_const, int lc, int keep, int32_t* sel_g, int sel_stride, int32_t* cnt_g,
+                      int32_t* sel_l, int32_t* len_l) {
+    pdl_trigger();
+    pdl_wait();
+    extern __shared__ __align__(16) unsigned char tsm[];
+    __shared__ TopkShared sh;
+    __shared__ int starts[kShardMaxRanks + 1];
+    const int m = blockIdx.x, M = gridDim.x, t = threadIdx.x, nt = blockDim.x;
+    if (t == 0) {
+        int acc = 0;
+        for (int r = 0; r < R; ++r) { starts[r] = acc; acc += counts[r * M + m]; }
+        starts[R] = acc;
+    }
+    __syncthreads();
+    const int64_t n = n_in ? n_in[m] : n_in_const;
+    const int cc = static_cast<int>((n + lc - 1) / lc);
+    const int K = keep / lc;
+    uint32_t* keys = reinterpret_cast<uint32_t*>(tsm);
+    int32_t* ssel = reinterpret_cast<int32_t*>(keys + ((R * W + 3) & ~3));
+    int nsel;
+    int64_t n_out;
+    if (n <= keep || cc <= K) {  // identity (pruning.cpp:159-168)
+        for (int j = t; j < cc; j += nt) ssel[j] = j;
+        nsel = cc;
+        n_out = n;
+        __syncthreads();
+    } else {
+        for (int j = t; j < cc; j += nt) {
+            int r = 0;
+            while (r + 1 < R && starts[r + 1] <= j) ++r;
+            keys[j] = order_key(__ldcg(gathered + (static_cast<int64_t>(r) * M + m) * W + (j - starts[r])));
+        }
+        __syncthreads();
+        cta_topk_smem(keys, cc, K, ssel, sh);
+        nsel = K;
+        n_out = static_cast<int64_t>(K - 1) * lc + min64(lc, n - static_cast<int64_t>(ssel[K - 1]) * lc);
+    }
+    for (int j = t; j < nsel; j += nt) sel_g[static_cast<int64_t>(m) * sel_stride + j] = ssel[j];
+    // this rank's part: the kept ids are ascending, so the ones in [lo, hi) are contiguous
+    const int lo = starts[rank], hi = starts[rank + 1];
+    int below = 0, inside = 0;
+    for (int j = 0; j < nsel; ++j) {  // nsel <= a few thousand: every thread scans (no barrier)
+        const int c = ssel[j];
+        below += c < lo;
+        inside += c >= lo && c < hi;
+    }
+    for (int j = t; j < inside; j += nt) sel_l[static_cast<int64_t>(m) * sel_stride + j] = ssel[below + j] - lo;
+    if (t == 0) {
+        cnt_g[m] = static_cast<int32_t>(n_out);
+        const int last = cc - 1;
+        const bool has_last = inside > 0 && ssel[below + inside - 1] == last && last >= lo && last < hi;
+        const int64_t tail = n - static_cast<int64_t>(last) * lc;
+        len_l[m] = static_cast<int32_t>(static_cast<int64_t>(inside) * lc - (has_last ? lc - tail : 0));
+    }
+}
+
+extern "C" int hp_select_topk_sharded(const float* gathered, const int32_t* counts, int32_t n_ranks, int32_t width,
+                                      int32_t rank, int32_t n_masks, const int32_t* n_in, int64_t n_in_const,
+                                      int32_t chunk_size, int32_t keep, int32_t* sel_global, int32_t sel_stride,
+                                      int32_t* count_global, int32_t* sel_local, int32_t* len_local, void* stream) {
+    if (!gathered || !counts || !sel_global || !count_global || !sel_local || !len_local || n_masks <= 0 || width <= 0)
+        return hph::set_error(HP_INVALID_ARGUMENT, "hp_select_topk_sharded: bad arguments");
+    if (n_ranks <= 0 || n_ranks > kShardMaxRanks || rank < 0 || rank >= n_ranks)
+        return hph::set_error(HP_INVALID_ARGUMENT, "hp_select_topk_sharded: rank %d of %d", rank, n_ranks);
+    if (chunk_size <= 0 || keep <= 0 || keep % chunk_size)
+        return hph::set_error(HP_INVALID_ARGUMENT, "StageConfig: k must be a positive multiple of l_c");
+    if (sel_stride < keep / chunk_size) return hph::set_error(HP_INVALID_ARGUMENT, "hp_select_topk_sharded: sel_stride < k/l_c");
+    const int64_t total = static_cast<int64_t>(n_ranks) * width;
+    if (total > kTopkMaxKeys)
+        return hph::set_error(HP_INVALID_ARGUMENT, "hp_select_topk_sharded: %lld chunks exceed the selection limit %d",
+                              static_cast<long long>(total), kTopkMaxKeys);
+    const size_t tsmem = static_cast<size_t>((total + 3) & ~3) * 4 + static_cast<size_t>(std::max<int64_t>(keep / chunk_size, total)) * 4;
+    cudaError_t e = cudaFuncSetAttribute(select_sharded_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(tsmem));
+    if (e == cudaSuccess)
+        e = launch_pdl(select_sharded_kernel, dim3(n_masks), dim3(kTopkThreads2), tsmem, static_cast<cudaStream_t>(stream),
+                       gathered, counts, n_ranks, width, rank, n_in, n_in_const, chunk_size, keep, sel_global, sel_stride,
+                       count_global, sel_local, len_local);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    return hph::check_cuda(e, "select_sharded_kernel");
+}
+
 extern "C" size_t hp_decode_bsa_workspace_bytes(int32_t n_q_heads, int32_t max_sel) {
     const int splits = std::max(1, (max_sel + kBsaMinKeys - 1) / kBsaMinKeys);  // bound for any keys/CTA
     return align_up(static_cast<size_t>(n_q_heads) * splits * kBsaRec * 4, 256) + align_up(static_cast<size_t>(n_q_heads) * 4, 256);

@@ -16,11 +16,14 @@ The only exchanges, per layer step:
     merge (hp_lse_merge).
 
 ``SeqShardLayer`` holds one rank's shard and exposes the step as phases (descend,
-select, attend, merge) around those two collectives. ``run_step`` drives the phases
-with a real process group (NCCL / gloo via torch.distributed); ``run_step_virtual``
-drives several shards inside one process (the single-GPU parity check). The pure
-host logic (shard geometry, assembling the gathered scores, slicing a rank's part of
-the global selection) is plain torch and runs on CPU too.
+select, attend, merge) around those two collectives; every phase is one kernel launch
+(select: hp_select_topk_sharded rebuilds the global score vector, selects, and cuts
+out the rank's part on the device). Every rank's score buffer has the same width,
+ceil(chunks / world), so the all-gather needs no padding step. ``run_step`` drives
+the phases with a real process group (NCCL; gloo through host memory for the 1-GPU
+multi-rank tests); ``run_step_virtual`` drives several shards inside one process (the
+single-GPU parity check). ``assemble``, ``local_part`` and ``lse_merge_reference``
+are torch restatements of the device steps for the CPU checks only.
 """
 from __future__ import annotations
 
@@ -82,7 +85,7 @@ class ShardGeometry:
 
 
 def assemble(gathered: torch.Tensor, counts: torch.Tensor, width: int) -> torch.Tensor:
-    """Concatenate per-rank segments in rank order, per mask.
+    """(CPU checker of hp_select_topk_sharded) concatenate per-rank segments in rank order, per mask.
 
     gathered [R, M, W] local scores (rank r's first counts[r, m] are valid),
     counts [R, M] -> [M, width] with row m = concat_r gathered[r, m, :counts[r, m]]
@@ -100,7 +103,7 @@ def assemble(gathered: torch.Tensor, counts: torch.Tensor, width: int) -> torch.
 
 
 def local_part(sel: torch.Tensor, k: torch.Tensor, lo: torch.Tensor, n: torch.Tensor):
-    """This rank's slice of a global ascending selection.
+    """(CPU checker of hp_select_topk_sharded) this rank's slice of a global ascending selection.
 
     sel [M, K] global chunk ids ascending (first k[m] valid), lo/n [M]: this rank owns
     global chunks [lo, lo + n). Returns (local ids [M, K] — the first cnt[m] valid —,
@@ -164,12 +167,11 @@ class SeqShardLayer:
         self.part_l = torch.zeros(n_q_heads, dtype=torch.float32, device=self.dev)
         self.part_o = torch.zeros((n_q_heads, 128), dtype=torch.float32, device=self.dev)
         # per stage: local scores (padded), global selection, this rank's slice of it
-        c0, c1 = geo.chunk_range()
         self.max_local = []
         prev_keep = None
         for i, (_, lc, keep) in enumerate(self.stages):
-            if i == 0:
-                self.max_local.append(max(1, c1 - c0))
+            if i == 0:  # the same width on every rank: the all-gather needs equal sizes
+                self.max_local.append(max(1, ceil_div(geo.cc1, geo.world)))
             else:
                 self.max_local.append(max(1, ceil_div(prev_keep, lc)))
             prev_keep = keep
@@ -177,8 +179,10 @@ class SeqShardLayer:
         self.sel_g = [torch.zeros((M, max(1, keep // lc)), dtype=torch.int32, device=self.dev)
                       for (_, lc, keep) in self.stages]
         self.cnt_g = [torch.zeros(M, dtype=torch.int32, device=self.dev) for _ in self.stages]
-        self.sel_l = [None] * len(self.stages)
-        self.len_l = [None] * len(self.stages)     # this rank's stage-(i+1) input length [M]
+        self.sel_l = [torch.zeros((M, max(1, keep // lc)), dtype=torch.int32, device=self.dev)
+                      for (_, lc, keep) in self.stages]  # this rank's kept chunks (local ids)
+        self.len_l = [torch.zeros(M, dtype=torch.int32, device=self.dev)
+                      for _ in self.stages]  # this rank's stage-(i+1) input length [M]
         self.ccl = [None] * len(self.stages)       # this rank's chunk count at stage i [M]
         self.g0 = [None] * len(self.stages)        # first global chunk of this rank at stage i [M]
         ws = max(lib().hp_decode_stage_workspace_bytes(M, w) for w in self.max_local)
@@ -211,7 +215,6 @@ class SeqShardLayer:
             in_count, const = count, 0
         ccl = (count + lc - 1) // lc
         self.ccl[i] = ccl
-        self.scores[i].fill_(float("-inf"))
         a = _capi.DecodeStageArgs(
             chunk_size=lc, keep=keep, n_masks=M, heads_per_mask=self.hpm, n_q_heads=self.n_q_heads,
             stream_tokens=self.geo.stream, q=self.q.data_ptr(), query_position=pos, in_=self._in_ref(i),
@@ -226,31 +229,22 @@ class SeqShardLayer:
         return self.scores[i], ccl.to(torch.int32)
 
     def select(self, i: int, gathered: torch.Tensor, counts: torch.Tensor, stream=None) -> None:
-        """Global stable top-K from every rank's scores, then this rank's slice of it."""
+        """Global stable top-K from every rank's scores [R, M, W] (chunk counts [R, M]),
+        and this rank's slice of it — one kernel (hp_select_topk_sharded)."""
         M = self.n_masks
         _, lc, keep = self.stages[i]
-        width = int(max(1, gathered.shape[0] * gathered.shape[2]))
-        total_in = self._global_input_len(i)
-        glob = assemble(gathered, counts, width).contiguous()
-        self._keep.append(glob)
-        check(lib().hp_select_topk(glob.data_ptr(), width, M, total_in.data_ptr(), 0, lc, keep,
-                                   self.sel_g[i].data_ptr(), self.sel_g[i].shape[1], self.cnt_g[i].data_ptr(),
-                                   C.c_void_p(_stream(stream))))
-        K = self.sel_g[i].shape[1]
-        kk = torch.minimum((total_in + lc - 1) // lc, torch.full_like(total_in, K))
-        starts = torch.cumsum(counts, 0) - counts
-        lo = starts[self.geo.rank].to(torch.int64)
-        n = counts[self.geo.rank].to(torch.int64)
-        loc, inside, below = local_part(self.sel_g[i].to(torch.int64), kk.to(torch.int64), lo, n)
-        self.sel_l[i] = loc.contiguous()
-        # this rank's output length: full chunks, except the globally last chunk may be short
-        last_global = ((total_in + lc - 1) // lc - 1).to(torch.int64)
-        has_last = ((self.sel_g[i].to(torch.int64) == last_global.unsqueeze(1)) &
-                    (torch.arange(K, device=self.dev) < kk.unsqueeze(1))).any(1) & \
-                   (last_global >= lo) & (last_global < lo + n)
-        tail = (total_in.to(torch.int64) - last_global * lc)
-        length = inside.to(torch.int64) * lc - torch.where(has_last, lc - tail, torch.zeros_like(tail))
-        self.len_l[i] = length.to(torch.int32)
+        R, _, W = gathered.shape
+        g = gathered.contiguous()
+        c = counts.to(torch.int32).contiguous()
+        self._keep += [g, c]
+        if i == 0:
+            n_in, n_const = None, self.geo.n0
+        else:
+            n_in, n_const = self.cnt_g[i - 1].data_ptr(), 0
+        check(lib().hp_select_topk_sharded(g.data_ptr(), c.data_ptr(), R, W, self.geo.rank, M, n_in, n_const, lc,
+                                           keep, self.sel_g[i].data_ptr(), self.sel_g[i].shape[1],
+                                           self.cnt_g[i].data_ptr(), self.sel_l[i].data_ptr(),
+                                           self.len_l[i].data_ptr(), C.c_void_p(_stream(stream))))
 
     def _global_input_len(self, i: int) -> torch.Tensor:
         M = self.n_masks
@@ -295,22 +289,31 @@ def _stream(stream=None) -> int:
 
 
 # ------------------------------------------------------------------- drivers
+def _all_gather(x: torch.Tensor, world: int, group=None) -> torch.Tensor:
+    """[world, *x.shape]: NCCL all_gather_into_tensor on the device; gloo (CPU process
+    groups — the multi-rank tests with every rank on one GPU) through host memory."""
+    import torch.distributed as dist
+    x = x.contiguous()
+    if dist.get_backend(group) == "nccl":
+        out = torch.empty((world,) + tuple(x.shape), dtype=x.dtype, device=x.device)
+        dist.all_gather_into_tensor(out, x, group=group)
+        return out
+    parts = [torch.empty_like(x, device="cpu") for _ in range(world)]
+    dist.all_gather(parts, x.cpu(), group=group)
+    return torch.stack(parts).to(x.device)
+
+
 def run_step(layer: SeqShardLayer, pos: int, group=None) -> torch.Tensor:
     """One decode layer step over a process group (NCCL over NVLink on a GPU box):
-    per stage an all-gather of chunk scores, then one of the (m, l, o) partials."""
-    import torch.distributed as dist
+    per stage an all-gather of chunk scores + chunk counts, then one of the (m, l, o)
+    partials. Every rank returns the merged output [n_q_heads, 128]."""
     world = layer.geo.world
     for i in range(len(layer.stages)):
         sc, cnt = layer.descend(i, pos)
-        g_sc = torch.empty((world,) + tuple(sc.shape), dtype=sc.dtype, device=sc.device)
-        g_cnt = torch.empty((world,) + tuple(cnt.shape), dtype=cnt.dtype, device=cnt.device)
-        dist.all_gather_into_tensor(g_sc, sc.contiguous(), group=group)
-        dist.all_gather_into_tensor(g_cnt, cnt.contiguous(), group=group)
-        layer.select(i, g_sc, g_cnt.to(torch.int64))
+        layer.select(i, _all_gather(sc, world, group), _all_gather(cnt, world, group))
     layer.attend(pos)
     parts = torch.cat([layer.part_m.unsqueeze(1), layer.part_l.unsqueeze(1), layer.part_o], 1)
-    g = torch.empty((world,) + tuple(parts.shape), dtype=parts.dtype, device=parts.device)
-    dist.all_gather_into_tensor(g, parts.contiguous(), group=group)
+    g = _all_gather(parts, world, group)
     return layer.merge(g[:, :, 0].contiguous(), g[:, :, 1].contiguous(), g[:, :, 2:].contiguous())
 
 
@@ -319,10 +322,8 @@ def run_step_virtual(layers: list[SeqShardLayer], pos: int) -> torch.Tensor:
     collectives become stacks of the shards' tensors."""
     for i in range(len(layers[0].stages)):
         outs = [ly.descend(i, pos) for ly in layers]
-        width = max(s.shape[1] for s, _ in outs)
-        g_sc = torch.stack([torch.nn.functional.pad(s, (0, width - s.shape[1]), value=float("-inf"))
-                            for s, _ in outs])
-        g_cnt = torch.stack([c for _, c in outs]).to(torch.int64)
+        g_sc = torch.stack([sc for sc, _ in outs])
+        g_cnt = torch.stack([c for _, c in outs])
         for ly in layers:
             ly.select(i, g_sc, g_cnt)
     for ly in layers:

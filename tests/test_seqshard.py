@@ -153,3 +153,91 @@ def test_sharded_decode_matches_unsharded(world, groups, t):
         assert sum((lists[r][m] for r in range(world)), []) == cl[m, : int(cc[m])].tolist()
     err = (got - want).abs().max().item() / want.abs().max().item()
     assert err <= 1e-3, err
+
+
+def _run_step_worker(rank, world, port, q, t, groups):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2502_08910_b200 import device as D, synth
+        torch.cuda.set_device(0)
+        hpm, d = 4, 128
+        stages = [(64, 256, 32768), (64, 32, 8192), (64, 8, 2048)]
+        qq, k, v = synth.generate(groups * hpm, groups, t, d, seed=31)
+        geo = S.ShardGeometry(t=t, sink=256, stream=1024, lc1=256, world=world, rank=rank)
+        t0, t1 = geo.token_range()
+        ly = S.SeqShardLayer(geo, k[:, t0:t1], v[:, t0:t1], stages, n_q_heads=groups * hpm, n_masks=groups)
+        ly.q.copy_(qq[:, 0])
+        got = S.run_step(ly, t - 1)  # the real multi-rank driver: all-gathers over the process group
+        full = D.FusedDecodeLayer(D.PagedKV(k, v), stages, sink=256, stream_tokens=1024,
+                                  n_q_heads=groups * hpm, n_masks=groups)
+        full.q.copy_(qq[:, 0])
+        want = full.run(t)
+        torch.cuda.synchronize()
+        ok = True
+        for i in range(3):
+            K = full.sel[i].shape[1]
+            ok &= bool(torch.equal(ly.sel_g[i][:, :K], full.sel[i])) and bool(torch.equal(ly.cnt_g[i], full.count[i]))
+        err = ((got - want).abs().max() / want.abs().max()).item()
+        q.put((rank, (ok and err <= 1e-3, err)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("t,groups", [(1 << 18, 8), (300_001, 2)])  # uneven chunk split across the ranks
+def test_run_step_multirank_world2(t, groups):
+    """seqshard.run_step with two real ranks (both on cuda:0, gloo): every stage's global
+    selection equals the unsharded layer's, the merged output within 1e-3."""
+    import socket
+    import torch.multiprocessing as mp
+    geo = S.ShardGeometry(t=t, sink=256, stream=1024, lc1=256, world=2, rank=0)
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_run_step_worker, args=(r, 2, port, q, t, groups)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=600) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert all(r[0] for r in res.values()), (res, geo.cc1)
+
+
+@pytest.mark.gpu
+def test_c5_3m_selection_matches_oracle(port):
+    """C5 context (3M tokens), one KV group, 8 virtual shards: the sharded step's final mask
+    equals the CPU oracle's (pruning.cpp:153-200 chained as decode.cpp:225-249)."""
+    from paper_2502_08910_b200 import synth
+    import ctypes as C
+    from paper_2502_08910_b200 import _capi
+    from paper_2502_08910_b200.device import _ref_push
+    t, groups, hpm, world = 3 << 20, 1, 4, 8
+    stages = [(64, 256, 32768), (64, 32, 8192), (64, 8, 2048)]
+    qq, k, v = synth.generate(groups * hpm, groups, t, 128, seed=41)
+    shards = []
+    for r in range(world):
+        geo = S.ShardGeometry(t=t, sink=256, stream=1024, lc1=256, world=world, rank=r)
+        t0, t1 = geo.token_range()
+        ly = S.SeqShardLayer(geo, k[:, t0:t1], v[:, t0:t1], stages, n_q_heads=groups * hpm, n_masks=groups)
+        ly.q.copy_(qq[:, 0])
+        shards.append(ly)
+    got = S.run_step_virtual(shards, t - 1)
+    torch.cuda.synchronize()
+    mask = []
+    for ly in shards:
+        ref = _ref_push(ly._in_ref(2), ly.sel_l[-1], stages[-1][1])
+        out = torch.zeros((groups, 2048), dtype=torch.int32, device="cuda")
+        _capi.check(_capi.lib().hp_decode_materialize((_capi.ListRef * 1)(ref), (C.c_void_p * 1)(ly.len_l[-1].data_ptr()),
+                                                      (C.c_void_p * 1)(out.data_ptr()), (C.c_int64 * 1)(2048), 1,
+                                                      groups, 2048, None))
+        torch.cuda.synchronize()
+        mask += out[0, : int(ly.len_l[-1][0])].tolist()
+    masks, want, _ = port.decode_layer_step(qq[:, 0].cpu().numpy().reshape(1, hpm, 128), k.float().cpu().numpy(),
+                                            v.float().cpu().numpy(), stages, sink=256, stream=1024)
+    assert mask == masks[0].tolist()
+    err = float(np.abs(got.cpu().numpy().reshape(1, hpm, 128) - want).max() / np.abs(want).max())
+    assert err <= 1e-3, err
