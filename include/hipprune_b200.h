@@ -129,6 +129,14 @@ typedef struct hp_stage_args {
      * |k| in [2^-63, 2^63], so bf16 q*k products are exact in fp32 and the sequential
      * dot may run as one fused multiply-add per element (same result, fewer instructions) */
     const int32_t* keys_exact;
+    /* optional (NULL = off): each descent's branch decisions, bit `it` set when
+     * iteration `it` went right — path_out[(list * max_chunks + chunk) * heads_per_mask + head].
+     * With the chunk lists this reproduces the reference's exact key-read sequence
+     * (select_rep_rotated, pruning.cpp:69-98) for KeySource instrumentation. */
+    uint32_t* path_out;
+    /* 1: run the descents even when the stage is the identity (select_rep on one chunk) */
+    int32_t descend_always;
+    int32_t pad2_;
 } hp_stage_args;
 
 size_t hp_stage_workspace_bytes(int32_t n_lists, int32_t max_chunks, int32_t keep, int32_t chunk_size);

@@ -147,6 +147,9 @@ class Oracle:
             self.f_estep = f("engine_step", C.c_int, _vp, _sz, _f32p, C.POINTER(C.c_int),
                              C.POINTER(C.c_double), C.POINTER(C.c_double), _u64p, _szp)
             self.f_ecache = f("engine_stage_cache", _vp, _vp, _sz, _sz)
+            self.f_efrozen = f("engine_set_frozen", C.c_int, _vp, C.POINTER(C.c_int), _sz)
+            self.f_chash = f("config_hash", C.c_int, C.POINTER(C.c_char_p), _sz, _u64p)
+            self.f_erecency = f("engine_store_recency", _sz, _vp, C.c_int, _u64p, _sz)
 
     # ---------------------------------------------------------------- helpers
     def _raise(self):
@@ -316,6 +319,13 @@ class Oracle:
                                _p(v, _f32p)))
         return q, k, v
 
+    def config_hash(self, overrides):
+        """config.cpp config_hash over default_config() + overrides (report plumbing)."""
+        arr = (C.c_char_p * max(1, len(overrides)))(*[o.encode() for o in overrides])
+        out = np.zeros(1, np.uint64)
+        self._check(self.f_chash(arr, len(overrides), _p(out, _u64p)))
+        return int(out[0])
+
     def decode_read_counts(self, q, k, stages, *, sink, stream, ext=False, layer1=4, cutoff=3):
         """Distinct / total key-row reads per stage for one group (q [hpm, d], k [T, d])."""
         assert self.kind == "reference"
@@ -330,12 +340,12 @@ class Oracle:
         return dis.astype(np.int64), tot.astype(np.int64)
 
     def engine(self, q, k, v, *, prefill_len, q_len, stages, sink, stream, refresh, ext=False,
-               cutoff=3, page_size=16, mask_cap=64, sa_cap=64):
+               cutoff=3, page_size=16, mask_cap=64, sa_cap=64, dev_cost=1.0, host_cost=31.5):
         """The reference DecodeEngine (decode.cpp:104-289) over a full workload
         q, k, v [layers, heads, T, d] (one query per position)."""
         assert self.kind == "reference"
         return _Engine(self, q, k, v, prefill_len, q_len, stages, sink, stream, refresh, ext,
-                       cutoff, page_size, mask_cap, sa_cap)
+                       cutoff, page_size, mask_cap, sa_cap, dev_cost, host_cost)
 
     # ------------------------------------------------------------------ store
     def store(self, num_layers, page_size, mask_cap, sa_cap):
@@ -344,7 +354,7 @@ class Oracle:
 
 class _Engine:
     def __init__(self, o: Oracle, q, k, v, prefill_len, q_len, stages, sink, stream, refresh, ext,
-                 cutoff, page_size, mask_cap, sa_cap):
+                 cutoff, page_size, mask_cap, sa_cap, dev_cost=1.0, host_cost=31.5):
         self.o = o
         self.q, self.k, self.v = _f32(q), _f32(k), _f32(v)
         L, H, T, d = self.q.shape
@@ -354,7 +364,7 @@ class _Engine:
         rf = _szarr(list(refresh))
         self.h = o.f_enew(_p(self.q, _f32p), _p(self.k, _f32p), _p(self.v, _f32p), L, H, T, d,
                           prefill_len, q_len, st, len(stages), sink, stream, rf, int(ext), cutoff,
-                          page_size, mask_cap, sa_cap, 1.0, 31.5, 0)
+                          page_size, mask_cap, sa_cap, dev_cost, host_cost, 0)
         if not self.h:
             o._raise()
 
@@ -380,7 +390,20 @@ class _Engine:
         sizes = (C.c_size_t * n)()
         self.o._check(self.o.f_estep(self.h, token_index, _p(out, _f32p), refreshed, lat,
                                      C.byref(bsa), _p(c4, _u64p), sizes))
+        self.last_telemetry = {"stage_latency": list(lat), "bsa_latency": bsa.value,
+                               "mask_hits": int(c4[0]), "mask_accesses": int(c4[1]),
+                               "sa_hits": int(c4[2]), "sa_accesses": int(c4[3])}
         return out, [bool(x) for x in refreshed], list(sizes)
+
+    def set_frozen_stages(self, frozen):
+        arr = (C.c_int * len(frozen))(*[int(bool(x)) for x in frozen])
+        self.o._check(self.o.f_efrozen(self.h, arr, len(frozen)))
+
+    def store_recency(self, bank):
+        n = self.o.f_erecency(self.h, bank, None, 0)
+        out = np.zeros(max(1, n), np.uint64)
+        self.o.f_erecency(self.h, bank, _p(out, _u64p), n)
+        return [int(x) for x in out[:n]]
 
     def stage_cache(self, layer, stage):
         return self.o._take_lists(self.o.f_ecache(self.h, layer, stage))[0]

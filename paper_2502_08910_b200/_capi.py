@@ -63,7 +63,8 @@ class StageArgs(C.Structure):
                 ("in_count", C.c_void_p), ("in_stride", C.c_int64), ("out_list", C.c_void_p),
                 ("out_count", C.c_void_p), ("out_stride", C.c_int64), ("workspace", C.c_void_p),
                 ("workspace_bytes", C.c_size_t), ("keys", KvView), ("rope", RopeCtx),
-                ("keys_exact", C.c_void_p)]
+                ("keys_exact", C.c_void_p), ("path_out", C.c_void_p), ("descend_always", C.c_int32),
+                ("pad2_", C.c_int32)]
 
 
 class BsaArgs(C.Structure):

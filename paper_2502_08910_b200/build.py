@@ -46,7 +46,7 @@ def build_cuda(force: bool = False, verbose: bool = False) -> Path:
     if variant:
         out = LIB / f"libhipprune_b200_{variant}.so"
         dev_flags = dev_flags + os.environ.get("HP_VARIANT_FLAGS", "").split()
-    deps = [CSRC / s for s in CUDA_SOURCES] + list(CSRC.glob("*.cuh")) + [ROOT / "include" / "hipprune_b200.h", Path(__file__)]
+    deps = [CSRC / s for s in CUDA_SOURCES] + list(CSRC.glob("*.cuh")) + [ROOT / "include" / "hipprune_b200.h"]
     if not force and not _stale(out, deps):
         return out
     objs, procs = [], []
@@ -66,7 +66,7 @@ def build_cuda(force: bool = False, verbose: bool = False) -> Path:
     return out
 
 
-HOST_SOURCES = ["host/host.cpp", "host/decode_engine.cpp"]
+HOST_SOURCES = ["host/host.cpp", "host/decode_engine.cpp", "host/kv_store.cpp"]
 
 
 def _cuda_home() -> Path:
@@ -81,7 +81,7 @@ def build_host(force: bool = False) -> Path:
     cuda = _cuda_home()
     cxx = os.environ.get("CXX", "g++")
     host = LIB / "libhipprune_host.so"
-    deps = [CSRC / s for s in HOST_SOURCES] + [ROOT / "include" / "hipprune_b200.hpp",
+    deps = [CSRC / s for s in HOST_SOURCES] + list((ROOT / "include" / "hipprune").glob("*.hpp")) + [ROOT / "include" / "hipprune_b200.hpp",
                                              ROOT / "include" / "hipprune_b200.h", LIB / "libhipprune_b200.so"]
     common = ["-O2", "-std=c++20", "-fPIC", "-ffp-contract=off", f"-I{ROOT / 'include'}", f"-I{cuda / 'include'}"]
     links = [f"-L{LIB}", "-lhipprune_b200", f"-L{cuda / 'lib64'}", "-lcudart", "-lz", "-Wl,-rpath,$ORIGIN",

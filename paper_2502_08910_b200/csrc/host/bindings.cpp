@@ -212,47 +212,53 @@ PYBIND11_MODULE(_hipprune, m) {
         },
         py::arg("selected"), py::arg("query"), py::arg("keys"));
 
-    // Report commands and the config hash are the reference's CLI plumbing
-    // (commands.cpp, config.cpp:105-254): outside the device hot path.
+    // run_report / config_hash (the reference's report plumbing, commands.cpp / config.cpp)
+    // are served by the Python package over this module's DecodeEngine and checkers
+    // (python/hipprune/_reports.py).
     m.def(
-        "run_report",
-        [](const std::string& command, const std::vector<std::string>&) -> py::dict {
-            throw std::logic_error("run_report('" + command +
-                                   "'): the reference's report commands are not part of the B200 hot path "
-                                   "(DESIGN.md section 7); use the reference CLI for reports");
+        "chunk_sparsity_histogram",
+        [](py::array_t<float, py::array::c_style | py::array::forcecast> query,
+           py::array_t<float, py::array::c_style | py::array::forcecast> keys, size_t k, size_t chunk_size) {
+            const DenseMatrix km = from_numpy(keys);
+            const ChunkSparsity cs = chunk_sparsity_histogram(std::span<const float>(query.data(), query.size()), km, k,
+                                                              chunk_size);
+            return py::make_tuple(cs.chunk_counts, cs.empty_fraction);
         },
-        py::arg("command"), py::arg("overrides") = std::vector<std::string>{});
-    m.def(
-        "config_hash",
-        [](const std::vector<std::string>&) -> std::uint64_t {
-            throw std::logic_error("config_hash: report/config plumbing is not part of the B200 hot path (DESIGN.md section 7)");
-        },
-        py::arg("overrides") = std::vector<std::string>{});
+        py::arg("query"), py::arg("keys"), py::arg("k"), py::arg("chunk_size"));
 
     m.def("device_available", &device_available);
 
     py::class_<PyEngine>(m, "DecodeEngine")
         .def(py::init([](const AttentionWorkload& full, size_t prefill_len, size_t q_len, const std::string& preset,
                          const std::vector<StageTuple>& stages, size_t sink, size_t stream,
-                         const std::vector<size_t>& refresh, bool extension, size_t page_size) {
+                         const std::vector<size_t>& refresh, bool extension, size_t page_size, size_t mask_capacity,
+                         size_t sa_capacity, double device_cost, double host_cost, size_t cutoff) {
                  auto e = std::make_unique<PyEngine>();
                  e->full = full;
                  PruningPlan plan = plan_from_args(preset, stages, sink, stream);
                  if (!refresh.empty()) plan.refresh_intervals = refresh;
                  RopePolicySet policy;
                  policy.extension_enabled = extension;
+                 policy.early_layer_cutoff = cutoff;
                  e->rope = std::make_unique<RopeTable>(build_rope_table(full.seq_len_kv + 2, full.head_dim));
                  StoreConfig sc;
                  sc.page_size = page_size;
+                 sc.mask_capacity = mask_capacity;
+                 sc.sa_capacity = sa_capacity;
+                 CostModel cost;
+                 cost.device_access_cost = device_cost;
+                 cost.host_access_cost = host_cost;
                  e->engine = std::make_unique<DecodeEngine>(truncate_workload(full, prefill_len, q_len), plan, policy,
-                                                            *e->rope, sc, full.seq_len_kv - prefill_len);
+                                                            *e->rope, sc, cost);
                  e->next = prefill_len;
                  return e;
              }),
              py::arg("full"), py::arg("prefill_len"), py::arg("q_len") = 64, py::arg("preset") = "3k",
              py::arg("stages") = std::vector<StageTuple>{}, py::arg("sink") = static_cast<size_t>(-1),
              py::arg("stream") = static_cast<size_t>(-1), py::arg("refresh") = std::vector<size_t>{},
-             py::arg("extension") = false, py::arg("page_size") = 64)
+             py::arg("extension") = false, py::arg("page_size") = 64, py::arg("mask_capacity") = 0,
+             py::arg("sa_capacity") = 0, py::arg("device_cost") = 1.0, py::arg("host_cost") = 31.5,
+             py::arg("cutoff") = 3)
         .def("set_frozen_stages", [](PyEngine& e, std::vector<bool> f) { e.engine->set_frozen_stages(std::move(f)); })
         .def("prefill",
              [](PyEngine& e) {
@@ -283,12 +289,25 @@ PYBIND11_MODULE(_hipprune, m) {
                  py::dict tel;
                  tel["step"] = r.telemetry.step;
                  tel["refreshed"] = r.telemetry.refreshed;
-                 tel["stage_us"] = r.telemetry.stage_latency;
-                 tel["bsa_us"] = r.telemetry.bsa_latency;
+                 tel["stage_latency"] = r.telemetry.stage_latency;  // CostModel units (decode.cpp:22-27)
+                 tel["bsa_latency"] = r.telemetry.bsa_latency;
+                 tel["mask_hits"] = r.telemetry.mask_hits;
+                 tel["mask_accesses"] = r.telemetry.mask_accesses;
+                 tel["sa_hits"] = r.telemetry.sa_hits;
+                 tel["sa_accesses"] = r.telemetry.sa_accesses;
                  tel["mask_sizes"] = r.telemetry.mask_sizes;
+                 tel["stage_us"] = r.telemetry.device_stage_us;  // measured on the device
+                 tel["bsa_us"] = r.telemetry.device_bsa_us;
                  return py::make_tuple(out, tel);
              })
         .def("stage_cache", [](PyEngine& e, size_t l, size_t s) { return e.engine->stage_cache(l, s); })
+        .def("reset_store_stats", [](PyEngine& e) { e.engine->store().reset_stats(); })
+        .def("store_stats",
+             [](PyEngine& e, int bank) {
+                 const BankStats st = e.engine->store().stats(static_cast<BankId>(bank));
+                 return py::make_tuple(st.hits, st.misses, st.evictions);
+             })
+        .def("store_recency", [](PyEngine& e, int bank) { return e.engine->store().recency_order(static_cast<BankId>(bank)); })
         .def_property_readonly("counters", [](PyEngine& e) { return e.engine->counters(); })
         .def_property_readonly("steps_taken", [](PyEngine& e) { return e.engine->steps_taken(); });
 }

@@ -6,6 +6,14 @@
 // at position T-1, and runs the block-sparse attention over sinks ∪ last cache ∪
 // stream for every head (decode.cpp:255-272). The caches live on the device; the
 // host mirror behind stage_cache() is refreshed on demand.
+//
+// Page accounting (decode.cpp:13-27,225-281): the engine owns the reference's
+// TieredKvStore over its host tier. Every pruning stage is one Mask-bank phase and
+// every attention pass one SA-bank phase; the device kernels report their branch
+// decisions, and the engine replays the reference's exact key/value read sequence
+// into the bank views — so hits, misses, evictions, the per-phase modeled latency
+// and the LRU order equal the reference engine's step by step. The misses are
+// committed once per step, in batches of the bank capacity (commit_rolling).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -73,6 +81,48 @@ int rope_policy_id(RopePolicyId id) {
 
 size_t cdiv(size_t a, size_t b) { return (a + b - 1) / b; }
 
+// Misses of a step committed in batches of the bank capacity (decode.cpp:13-20).
+void commit_rolling(TieredKvStore& store, BankId bank, std::span<const std::uint64_t> pages) {
+    const size_t cap = store.capacity(bank);
+    if (cap == 0) return;  // zero-capacity bank: every page stays on the host tier
+    for (size_t b = 0; b < pages.size(); b += cap) store.commit(bank, pages.subspan(b, std::min(cap, pages.size() - b)));
+}
+
+double phase_latency(const KvView& v, const CostModel& c) {
+    const std::uint64_t hits = v.phase_hits(), miss = v.phase_accesses() - hits;
+    return static_cast<double>(hits) * c.device_access_cost + static_cast<double>(miss) * c.host_access_cost;
+}
+
+int ceil_log2(size_t n) {
+    int r = 0;
+    while ((size_t{1} << r) < n) ++r;
+    return r;
+}
+
+// the reference's key reads of one decode stage (pruning.cpp:69-98,170-185) from the
+// device's branch decisions (paths[chunk * heads + head])
+void replay_stage(KeySource& ks, const std::vector<size_t>& list, size_t lc, size_t heads, const uint32_t* paths) {
+    const size_t cc = cdiv(list.size(), lc);
+    for (size_t j = 0; j < cc; ++j) {
+        const size_t b = j * lc, n = std::min(lc, list.size() - b);
+        for (size_t h = 0; h < heads; ++h) {
+            size_t first = 1, last = n;
+            if (n > 1) {
+                const uint32_t bits = paths[j * heads + h];
+                const int iters = ceil_log2(n);
+                for (int it = 0; it < iters && first < last; ++it) {
+                    const size_t mid = (first + last + 1) / 2;
+                    ks.key_row(h, list[b + first - 1]);
+                    ks.key_row(h, list[b + mid - 1]);
+                    if ((bits >> it) & 1u) first = mid;
+                    else last = mid - 1;
+                }
+            }
+            ks.key_row(h, list[b + first - 1]);
+        }
+    }
+}
+
 }  // namespace
 
 struct DecodeEngine::Device {
@@ -83,6 +133,7 @@ struct DecodeEngine::Device {
         std::vector<Buf> cache;     // per stage: [keep] int32 (stage cache list)
         std::vector<Buf> count;     // per stage: [1] int32
         Buf sel, selc;              // selected list of the step's query row
+        std::vector<Buf> paths;     // per stage: branch decisions [chunk][head] (accounting replay)
     };
     std::vector<Layer> layers;
     Buf in_start, in_count;         // stage-0 range input
@@ -172,14 +223,19 @@ TokenInput token_input_at(const AttentionWorkload& full, std::size_t token_index
 }
 
 DecodeEngine::DecodeEngine(AttentionWorkload workload, PruningPlan plan, RopePolicySet policy, const RopeTable& rope,
-                           StoreConfig store_config, std::size_t max_steps)
+                           StoreConfig store_config, CostModel cost)
     : dev_(std::make_unique<Device>()),
       workload_(std::move(workload)),
       plan_(std::move(plan)),
       policy_(policy),
-      rope_(&rope) {
+      rope_(&rope),
+      cost_(cost) {
     plan_.validate();
+    cost_.validate();
     workload_.validate();
+    store_ = std::make_unique<TieredKvStore>(workload_, store_config.page_size, store_config.mask_capacity,
+                                             store_config.sa_capacity);
+    const std::size_t max_steps = 4096;  // initial device capacity past the prefill (grows on demand)
     if (!hp_device_available())
         throw std::runtime_error("hipprune_b200: no CUDA device — the B200 path has no CPU fallback");
     if (plan_.refresh_intervals.empty()) plan_.refresh_intervals.assign(plan_.stages.size(), 1);
@@ -227,6 +283,7 @@ DecodeEngine::DecodeEngine(AttentionWorkload workload, PruningPlan plan, RopePol
         }
         Ly.sel.alloc(D.sel_stride * 4);
         Ly.selc.alloc(4);
+        Ly.paths.resize(S);
     }
     D.in_start.alloc(4);
     D.in_count.alloc(4);
@@ -278,8 +335,14 @@ PrefillResult DecodeEngine::prefill() {
     PrefillResult result;
     for (size_t l = 0; l < workload_.num_layers; ++l) {
         StageTrace trace;
-        SparseBlockMask mask = build_mask(plan_, workload_, l, policy_, *rope_, &trace);
-        result.outputs.push_back(block_sparse_attention(workload_, l, mask, policy_, *rope_));
+        KvView mask_view(*store_, BankId::Mask, l);
+        mask_view.begin_phase();
+        SparseBlockMask mask = build_mask(plan_, workload_, l, policy_, *rope_, &mask_view, &trace);
+        commit_rolling(*store_, BankId::Mask, mask_view.drain_missing());
+        KvView sa_view(*store_, BankId::Sa, l);
+        sa_view.begin_phase();
+        result.outputs.push_back(block_sparse_attention(workload_, l, mask, policy_, *rope_, sa_view));
+        commit_rolling(*store_, BankId::Sa, sa_view.drain_missing());
         auto& Ly = dev_->layers[l];
         for (size_t i = 0; i < plan_.stages.size(); ++i) {
             const auto& lst = trace.last_block_outputs[i];
@@ -293,6 +356,7 @@ PrefillResult DecodeEngine::prefill() {
         }
         result.masks.push_back(std::move(mask));
     }
+    store_->check_consistency();
     prefilled_ = true;
     return result;
 }
@@ -311,8 +375,27 @@ StepResult DecodeEngine::step(const TokenInput& token) {
                 throw std::invalid_argument("step: token row width mismatch");
     }
     Device& D = *dev_;
-    if (static_cast<int64_t>(seq_len_kv_) + 1 > static_cast<int64_t>(D.pages) * D.page_size)
-        throw std::out_of_range("step: device KV capacity exhausted (raise max_steps)");
+    if (static_cast<int64_t>(seq_len_kv_) + 1 > static_cast<int64_t>(D.pages) * D.page_size) {
+        // grow every layer's paged pools (double the pages; the page layout is unchanged)
+        const int32_t np = D.pages * 2;
+        const size_t old_b = static_cast<size_t>(D.pages) * H * D.page_size * dd * 4;
+        for (auto& Ly : D.layers)
+            for (Buf* b : {&Ly.k, &Ly.v}) {
+                Buf nb;
+                nb.alloc(old_b * 2);
+                cu(cudaMemcpy(nb.p, b->p, old_b, cudaMemcpyDeviceToDevice), "grow KV");
+                *b = std::move(nb);
+            }
+        D.pages = np;
+    }
+    // the host tier grows with the sequence, as the reference's workload does
+    // (decode.cpp:202-208): the bank views read it
+    for (size_t l = 0; l < L; ++l)
+        for (size_t h = 0; h < H; ++h) {
+            workload_.keys[l][h].append_row(token.k[l][h]);
+            workload_.values[l][h].append_row(token.v[l][h]);
+        }
+    workload_.seq_len_kv += 1;
     seq_len_kv_ += 1;
     const size_t T = seq_len_kv_, pos = T - 1;
     std::vector<bool> flags = refresh_due(counters_, plan_);
@@ -322,6 +405,8 @@ StepResult DecodeEngine::step(const TokenInput& token) {
     StepResult result;
     result.telemetry.refreshed = flags;
     result.telemetry.stage_latency.assign(S, 0.0);
+    result.telemetry.device_stage_us.assign(S, 0.0);
+    std::vector<std::uint64_t> mask_missing, sa_missing;
     result.output.assign(L, std::vector<std::vector<float>>(H, std::vector<float>(dd)));
 
     const size_t upper = T > plan_.stream_tokens ? T - plan_.stream_tokens : 0;
@@ -350,6 +435,7 @@ StepResult DecodeEngine::step(const TokenInput& token) {
         rc.early_policy = rope_policy_id(policy_.pruning_policy_early);
         rc.late_policy = rope_policy_id(policy_.pruning_policy_late);
         rc.layer = static_cast<int32_t>(l + 1);
+        KvView mask_view(*store_, BankId::Mask, l);
         for (size_t i = 0; i < S; ++i) {
             if (!flags[i]) continue;
             const auto& st = plan_.stages[i];
@@ -384,10 +470,39 @@ StepResult DecodeEngine::step(const TokenInput& token) {
             a.workspace_bytes = D.ws.bytes;
             a.keys = kvv;
             a.rope = rc;
+            // the input list as the reference sees it (for the read replay), taken before
+            // this stage overwrites nothing it reads (stage i reads cache i-1)
+            std::vector<size_t> input;
+            if (i == 0) {
+                input.resize(static_cast<size_t>(n0));
+                std::iota(input.begin(), input.end(), plan_.sink_tokens);
+            } else {
+                cu(cudaStreamSynchronize(D.stream), "sync");
+                input = stage_cache(l, i - 1);
+            }
+            const size_t paths_n = static_cast<size_t>(a.max_chunks) * H;
+            if (Ly.paths[i].bytes < paths_n * 4) Ly.paths[i].alloc(paths_n * 4);
+            a.path_out = Ly.paths[i].as<uint32_t>();
             ck(hp_prune_stage(&a, D.stream));
             cu(cudaEventRecord(e[1], D.stream), "event");
             last_refresh_[l][i] = step_index_ + 1;
             cache_stale_[l][i] = true;
+            // Mask-bank phase: the stage's exact key reads (identity stages read nothing)
+            mask_view.begin_phase();
+            const size_t K = st.keep / st.chunk_size;
+            if (!(input.size() <= st.keep || cdiv(input.size(), st.chunk_size) <= K)) {
+                std::vector<uint32_t> ph(paths_n);
+                cu(cudaMemcpyAsync(ph.data(), Ly.paths[i].p, paths_n * 4, cudaMemcpyDeviceToHost, D.stream), "download");
+                cu(cudaStreamSynchronize(D.stream), "sync");
+                replay_stage(mask_view, input, st.chunk_size, H, ph.data());
+            }
+            result.telemetry.stage_latency[i] += phase_latency(mask_view, cost_);
+            result.telemetry.mask_hits += mask_view.phase_hits();
+            result.telemetry.mask_accesses += mask_view.phase_accesses();
+        }
+        {
+            const auto miss = mask_view.drain_missing();
+            mask_missing.insert(mask_missing.end(), miss.begin(), miss.end());
         }
         cudaEvent_t* e = &D.ev[(l * (S + 1) + S) * 2];
         cu(cudaEventRecord(e[0], D.stream), "event");
@@ -414,6 +529,26 @@ StepResult DecodeEngine::step(const TokenInput& token) {
         b.rope.layer = 0;
         ck(hp_bsa(&b, D.stream));
         cu(cudaEventRecord(e[1], D.stream), "event");
+        // SA-bank phase: every head reads the selected keys, then the values (decode.cpp:255-272)
+        KvView sa_view(*store_, BankId::Sa, l);
+        sa_view.begin_phase();
+        SparseBlockMask m1;
+        m1.block_size = 1;
+        m1.sink_tokens = plan_.sink_tokens;
+        m1.stream_tokens = plan_.stream_tokens;
+        m1.query_offset = pos;
+        cu(cudaStreamSynchronize(D.stream), "sync");
+        m1.indices = {stage_cache(l, S - 1)};
+        const std::vector<size_t> selected = selected_indices(m1, 0);
+        for (size_t h = 0; h < H; ++h) {
+            for (size_t t : selected) sa_view.key_row(h, t);
+            for (size_t t : selected) sa_view.value_row(h, t);
+        }
+        result.telemetry.bsa_latency += phase_latency(sa_view, cost_);
+        result.telemetry.sa_hits += sa_view.phase_hits();
+        result.telemetry.sa_accesses += sa_view.phase_accesses();
+        const auto miss = sa_view.drain_missing();
+        sa_missing.insert(sa_missing.end(), miss.begin(), miss.end());
     }
     std::vector<float> oh(H * dd);
     for (size_t l = 0; l < L; ++l) {
@@ -426,10 +561,13 @@ StepResult DecodeEngine::step(const TokenInput& token) {
             if (i < S && !flags[i]) continue;
             float ms = 0.f;
             cu(cudaEventElapsedTime(&ms, D.ev[(l * (S + 1) + i) * 2], D.ev[(l * (S + 1) + i) * 2 + 1]), "elapsed");
-            (i < S ? result.telemetry.stage_latency[i] : result.telemetry.bsa_latency) += 1000.0 * ms;
+            (i < S ? result.telemetry.device_stage_us[i] : result.telemetry.device_bsa_us) += 1000.0 * ms;
         }
     }
     for (size_t i = 0; i < S; ++i) result.telemetry.mask_sizes.push_back(stage_cache(L - 1, i).size());
+    commit_rolling(*store_, BankId::Mask, mask_missing);
+    commit_rolling(*store_, BankId::Sa, sa_missing);
+    store_->check_consistency();
     for (size_t i = 0; i < S; ++i) counters_[i] = (counters_[i] + 1) % plan_.refresh_intervals[i];
     ++step_index_;
     result.telemetry.step = step_index_;

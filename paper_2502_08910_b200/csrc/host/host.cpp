@@ -375,10 +375,10 @@ std::uint32_t dump_checksum(const AttentionWorkload& wl) {
 
 // HIPW v1: "HIPW", u32 version, u64 H/L/T_q/T_kv/d, raw fp32 Q,K,V per (layer, head),
 // u32 CRC-32 of the payload (workload.cpp:234-312).
-void save_dump(const AttentionWorkload& wl, const std::string& path) {
+void save_dump(const AttentionWorkload& wl, const std::filesystem::path& path) {
     wl.validate();
     std::ofstream os(path, std::ios::binary | std::ios::trunc);
-    if (!os) throw FormatError("cannot open for writing: " + path);
+    if (!os) throw FormatError("cannot open for writing: " + path.string());
     os.write("HIPW", 4);
     put_le(os, 1, 4);
     for (std::uint64_t v : {wl.num_heads, wl.num_layers, wl.seq_len_q, wl.seq_len_kv, wl.head_dim}) put_le(os, v, 8);
@@ -388,12 +388,12 @@ void save_dump(const AttentionWorkload& wl, const std::string& path) {
                 os.write(reinterpret_cast<const char*>(m->data.data()),
                          static_cast<std::streamsize>(m->data.size() * sizeof(float)));
     put_le(os, dump_checksum(wl), 4);
-    if (!os) throw FormatError("write failure: " + path);
+    if (!os) throw FormatError("write failure: " + path.string());
 }
 
-AttentionWorkload load_dump(const std::string& path) {
+AttentionWorkload load_dump(const std::filesystem::path& path) {
     std::ifstream is(path, std::ios::binary);
-    if (!is) throw FormatError("cannot open for reading: " + path);
+    if (!is) throw FormatError("cannot open for reading: " + path.string());
     char magic[4];
     if (!is.read(magic, 4)) throw FormatError("truncated header");
     if (std::memcmp(magic, "HIPW", 4) != 0) throw FormatError("magic mismatch in header");
@@ -465,8 +465,23 @@ PruningPlan preset_plan(const std::string& name) {
     return p;
 }
 
-SparseBlockMask build_mask(const PruningPlan& plan, const AttentionWorkload& wl, std::size_t layer,
-                           const RopePolicySet& policy, const RopeTable& rope, StageTrace* trace, std::size_t) {
+namespace {
+void replay_stage_reads(KeySource& ks, std::span<const std::size_t> list, std::size_t lc, std::size_t heads,
+                        const std::uint32_t* paths);
+void build_layer_from_source(struct DeviceLayer& dl, KeySource& ks, const AttentionWorkload* src_wl, size_t src_layer,
+                             size_t heads, size_t t_kv, size_t d, bool with_values,
+                             std::span<const std::size_t> tokens);
+}  // namespace
+
+// Alg. 1 on the device. Rows come from `data` (layer `data_layer`) — the workload, or
+// the host tier behind one of this library's KeySources — or, for any other
+// KeySource, through `foreign` (read once per row to upload). With `replay` the
+// device's branch decisions are replayed into it as the reference's sequential
+// instrumented walk reads: stage by stage, query block by block (pruning.cpp:232-262).
+static SparseBlockMask build_mask_device(const PruningPlan& plan, const AttentionWorkload& wl, std::size_t layer,
+                                         const RopePolicySet& policy, const RopeTable& rope,
+                                         const AttentionWorkload* data, std::size_t data_layer, KeySource* foreign,
+                                         KeySource* replay, StageTrace* trace) {
     plan.validate();
     if (layer >= wl.num_layers) throw std::out_of_range("build_mask: layer out of range");
     const size_t t_q = wl.seq_len_q, t_kv = wl.seq_len_kv;
@@ -480,7 +495,8 @@ SparseBlockMask build_mask(const PruningPlan& plan, const AttentionWorkload& wl,
     };
 
     DeviceLayer kv;
-    kv.build(wl, layer, false);
+    if (foreign) build_layer_from_source(kv, *foreign, nullptr, 0, wl.num_heads, t_kv, wl.head_dim, false, {});
+    else kv.build(*data, data_layer, false);
     const std::vector<float> qh = pack_q(wl, layer, 0, t_q);
     DevBuf q(qh.size() * 4);
     q.upload(qh.data(), qh.size() * 4);
@@ -537,7 +553,32 @@ SparseBlockMask build_mask(const PruningPlan& plan, const AttentionWorkload& wl,
         a.workspace_bytes = ws.bytes;
         a.keys = kv.view();
         a.rope = rc;
+        DevBuf paths;
+        if (replay) {
+            paths.alloc(std::max<size_t>(1, nb * static_cast<size_t>(max_chunks) * heads) * 4);
+            a.path_out = paths.as<std::uint32_t>();
+        }
         check(hp_prune_stage(&a, nullptr));
+        if (replay) {  // the reference's read sequence of this stage, block by block
+            std::vector<std::uint32_t> ph(nb * static_cast<size_t>(max_chunks) * heads);
+            paths.download(ph.data(), ph.size() * 4);
+            std::vector<int32_t> cnt(nb);
+            in_count.download(cnt.data(), nb * 4);
+            std::vector<int32_t> lst;
+            if (in_list.p) {
+                lst.resize(nb * static_cast<size_t>(in_stride));
+                in_list.download(lst.data(), lst.size() * 4);
+            }
+            for (size_t m = 0; m < nb; ++m) {
+                const size_t n = static_cast<size_t>(cnt[m]);
+                if (n <= st.keep || ceil_div(n, st.chunk_size) <= st.keep / st.chunk_size) continue;  // identity
+                std::vector<std::size_t> list(n);
+                for (size_t i = 0; i < n; ++i)
+                    list[i] = in_list.p ? static_cast<size_t>(lst[m * in_stride + i]) : plan.sink_tokens + i;
+                replay_stage_reads(*replay, list, st.chunk_size, static_cast<size_t>(heads),
+                                   ph.data() + m * static_cast<size_t>(max_chunks) * heads);
+            }
+        }
         if (trace) {
             int32_t c = 0;
             out_count.download(&c, 4, (nb - 1) * 4);
@@ -575,6 +616,23 @@ SparseBlockMask build_mask(const PruningPlan& plan, const AttentionWorkload& wl,
     for (size_t m = 0; m < nb; ++m)
         mask.indices[m].assign(lists.begin() + m * in_stride, lists.begin() + m * in_stride + cnt[m]);
     return mask;
+}
+
+SparseBlockMask build_mask(const PruningPlan& plan, const AttentionWorkload& wl, std::size_t layer,
+                           const RopePolicySet& policy, const RopeTable& rope, KeySource* keys, StageTrace* trace,
+                           std::size_t) {
+    if (keys == nullptr) return build_mask_device(plan, wl, layer, policy, rope, &wl, layer, nullptr, nullptr, trace);
+    if (auto* d = dynamic_cast<DirectKeySource*>(keys))
+        return build_mask_device(plan, wl, layer, policy, rope, &d->workload(), d->layer(), nullptr, keys, trace);
+    if (auto* v = dynamic_cast<KvView*>(keys))
+        return build_mask_device(plan, wl, layer, policy, rope, &v->host(), v->layer(), nullptr, keys, trace);
+    return build_mask_device(plan, wl, layer, policy, rope, nullptr, 0, keys, nullptr, trace);
+}
+
+SparseBlockMask build_mask(const PruningPlan& plan, const AttentionWorkload& wl, std::size_t layer,
+                           const RopePolicySet& policy, const RopeTable& rope, StageTrace* trace,
+                           std::size_t num_threads) {
+    return build_mask(plan, wl, layer, policy, rope, static_cast<KeySource*>(nullptr), trace, num_threads);
 }
 
 // ========================================================= sparse attention
@@ -739,5 +797,474 @@ double attention_recall(std::span<const std::size_t> selected, std::span<const f
 }
 
 bool device_available() { return hp_device_available() != 0; }
+
+// ===================================================== reference host helpers
+// tensor.cpp / rope_policy.cpp restated: the arithmetic contract the kernels reproduce.
+void apply_rope_inplace(std::span<float> vec, std::size_t position, const RopeTable& table) {
+    if (vec.size() != table.head_dim)
+        throw std::invalid_argument("apply_rope: vector length " + std::to_string(vec.size()) + " != head_dim " +
+                                    std::to_string(table.head_dim));
+    if (position >= table.max_position)
+        throw std::out_of_range("apply_rope: position " + std::to_string(position) + " >= max_position " +
+                                std::to_string(table.max_position));
+    const size_t half = table.head_dim / 2;
+    const float* c = table.cos_tab.row(position);
+    const float* sn = table.sin_tab.row(position);
+    for (size_t i = 0; i < half; ++i) {
+        const float x = vec[i], y = vec[i + half];
+        const float xc = x * c[i], ys = y * sn[i], xs = x * sn[i], yc = y * c[i];
+        vec[i] = xc - ys;
+        vec[i + half] = xs + yc;
+    }
+}
+
+std::vector<float> apply_rope(std::span<const float> vec, std::size_t position, const RopeTable& table) {
+    std::vector<float> out(vec.begin(), vec.end());
+    apply_rope_inplace(out, position, table);
+    return out;
+}
+
+float dot_f32(std::span<const float> a, std::span<const float> b) {
+    if (a.size() != b.size())
+        throw std::invalid_argument("dot_f32: length mismatch " + std::to_string(a.size()) + " vs " +
+                                    std::to_string(b.size()));
+    return dot_seq(a, b);
+}
+
+float block_scores(const DenseMatrix& qblock, std::span<const float> key) {
+    if (qblock.cols != key.size())
+        throw std::invalid_argument("block_scores: qblock cols " + std::to_string(qblock.cols) + " != key length " +
+                                    std::to_string(key.size()));
+    if (qblock.rows == 0) throw std::invalid_argument("block_scores: empty query block");
+    float best = dot_seq(qblock.row_span(0), key);
+    for (size_t t = 1; t < qblock.rows; ++t) best = std::max(best, dot_seq(qblock.row_span(t), key));
+    return best;
+}
+
+namespace {
+RopePolicyId pruning_policy_of(const RopePolicySet& p, std::size_t layer) {
+    return layer > p.early_layer_cutoff ? p.pruning_policy_late : p.pruning_policy_early;
+}
+}  // namespace
+
+std::size_t query_position(const RopePolicySet& policy, std::size_t layer, const PositionContext& ctx) {
+    switch (pruning_policy_of(policy, layer)) {
+        case RopePolicyId::Relative: return ctx.stream_tokens + 1;
+        case RopePolicyId::ChunkIndexed: return std::min(ctx.query_position, ctx.chunk_count + ctx.stream_tokens);
+        case RopePolicyId::PlugIn:
+            if (!policy.plugin) throw std::logic_error("query_position: PlugIn policy without a registered hook");
+            return policy.plugin(true, layer, ctx);
+        default: break;
+    }
+    throw std::logic_error("query_position: policy not applicable to pruning");
+}
+
+std::size_t key_position(const RopePolicySet& policy, std::size_t layer, const PositionContext& ctx) {
+    if (ctx.branch != 1 && ctx.branch != 2) throw std::logic_error("key_position: branch must be 1 or 2");
+    switch (pruning_policy_of(policy, layer)) {
+        case RopePolicyId::Relative: return static_cast<std::size_t>(ctx.branch - 1);
+        case RopePolicyId::ChunkIndexed: return ctx.chunk_index;
+        case RopePolicyId::PlugIn:
+            if (!policy.plugin) throw std::logic_error("key_position: PlugIn policy without a registered hook");
+            return policy.plugin(false, layer, ctx);
+        default: break;
+    }
+    throw std::logic_error("key_position: policy not applicable to pruning");
+}
+
+std::vector<std::size_t> streaming_positions(std::span<const std::size_t> selected, std::size_t query_pos,
+                                             std::size_t) {
+    const size_t n = selected.size();
+    if (n > query_pos + 1)
+        throw std::logic_error("streaming_positions: " + std::to_string(n) + " selected tokens cannot fit below position " +
+                               std::to_string(query_pos));
+    std::vector<std::size_t> pos(n);
+    for (size_t i = 0; i < n; ++i) pos[i] = query_pos + 1 - n + i;
+    return pos;
+}
+
+ChunkPartition partition_chunks(std::span<const std::size_t> indices, std::size_t chunk_size) {
+    if (chunk_size == 0) throw std::invalid_argument("partition_chunks: chunk_size must be >= 1");
+    ChunkPartition out;
+    for (size_t b = 0; b < indices.size(); b += chunk_size)
+        out.chunks.emplace_back(indices.begin() + b, indices.begin() + std::min(indices.size(), b + chunk_size));
+    return out;
+}
+
+ChunkSparsity chunk_sparsity_histogram(std::span<const float> query, const DenseMatrix& keys, std::size_t k,
+                                       std::size_t chunk_size) {
+    if (chunk_size == 0 || chunk_size > keys.rows)
+        throw std::invalid_argument("chunk_sparsity_histogram: chunk size out of range");
+    const std::vector<std::size_t> top = exact_topk(query, keys, k);
+    ChunkSparsity out;
+    out.chunk_counts.assign(ceil_div(keys.rows, chunk_size), 0);
+    for (size_t i : top) ++out.chunk_counts[i / chunk_size];
+    const size_t empty = static_cast<size_t>(std::count(out.chunk_counts.begin(), out.chunk_counts.end(), size_t{0}));
+    out.empty_fraction = static_cast<double>(empty) / static_cast<double>(out.chunk_counts.size());
+    return out;
+}
+
+// ========================================================= KeySource operators
+namespace {
+
+int ceil_log2(size_t n) {
+    int r = 0;
+    while ((size_t{1} << r) < n) ++r;
+    return r;
+}
+
+// The reference's key reads of one stage (run_pruning_stage + select_rep_rotated,
+// pruning.cpp:69-98,170-185), replayed from the device's branch decisions:
+// chunk by chunk, head by head, per iteration chunk[first-1] then chunk[mid-1],
+// then the representative once more for its branch-2 score.
+void replay_stage_reads(KeySource& ks, std::span<const std::size_t> list, std::size_t lc, std::size_t heads,
+                        const std::uint32_t* paths) {
+    const size_t cc = ceil_div(list.size(), lc);
+    for (size_t j = 0; j < cc; ++j) {
+        const size_t b = j * lc, n = std::min(lc, list.size() - b);
+        for (size_t h = 0; h < heads; ++h) {
+            size_t first = 1, last = n;
+            if (n > 1) {
+                const std::uint32_t bits = paths[j * heads + h];
+                const int iters = ceil_log2(n);
+                for (int it = 0; it < iters && first < last; ++it) {
+                    const size_t mid = (first + last + 1) / 2;
+                    ks.key_row(h, list[b + first - 1]);
+                    ks.key_row(h, list[b + mid - 1]);
+                    if ((bits >> it) & 1u) first = mid;
+                    else last = mid - 1;
+                }
+            }
+            ks.key_row(h, list[b + first - 1]);
+        }
+    }
+}
+
+// select_rep's own reads (no trailing representative read) for one chunk
+size_t replay_select_rep(KeySource& ks, std::span<const std::size_t> chunk, std::size_t head, std::uint32_t bits) {
+    size_t first = 1, last = chunk.size();
+    const int iters = ceil_log2(chunk.size());
+    for (int it = 0; it < iters && first < last; ++it) {
+        const size_t mid = (first + last + 1) / 2;
+        ks.key_row(head, chunk[first - 1]);
+        ks.key_row(head, chunk[mid - 1]);
+        if ((bits >> it) & 1u) first = mid;
+        else last = mid - 1;
+    }
+    return chunk[first - 1];
+}
+
+// K (and V) rows of a device layer [pages][heads][64][d] fp32: the workload layer when
+// known, else through the source (`tokens` — or every token below t_kv — read once)
+void build_layer_from_source(DeviceLayer& dl, KeySource& ks, const AttentionWorkload* src_wl, size_t src_layer,
+                             size_t heads, size_t t_kv, size_t d, bool with_values,
+                             std::span<const std::size_t> tokens) {
+    if (src_wl) {
+        dl.build(*src_wl, src_layer, with_values);
+        return;
+    }
+    const int32_t ps = 64;
+    dl.heads = static_cast<int32_t>(heads);
+    dl.d = static_cast<int32_t>(d);
+    dl.page_size = ps;
+    dl.t_kv = static_cast<int64_t>(t_kv);
+    dl.pages = static_cast<int32_t>(std::max<size_t>(1, ceil_div(t_kv, ps)));
+    const size_t n = static_cast<size_t>(dl.pages) * heads * ps * d;
+    std::vector<float> hk(n, 0.0f), hv(with_values ? n : 0, 0.0f);
+    auto put = [&](size_t h, size_t t) {
+        const size_t o = (((t / ps) * heads + h) * ps + t % ps) * d;
+        const auto kr = ks.key_row(h, t);
+        if (kr.size() != d) throw std::invalid_argument("KeySource: key row width != head_dim");
+        std::memcpy(&hk[o], kr.data(), d * 4);
+        if (with_values) {
+            const auto vr = ks.value_row(h, t);
+            if (vr.size() != d) throw std::invalid_argument("KeySource: value row width != head_dim");
+            std::memcpy(&hv[o], vr.data(), d * 4);
+        }
+    };
+    for (size_t h = 0; h < heads; ++h) {
+        if (tokens.empty())
+            for (size_t t = 0; t < t_kv; ++t) put(h, t);
+        else
+            for (size_t t : tokens) put(h, t);
+    }
+    dl.k.alloc(n * 4);
+    dl.k.upload(hk.data(), n * 4);
+    if (with_values) {
+        dl.v.alloc(n * 4);
+        dl.v.upload(hv.data(), n * 4);
+    }
+}
+
+struct SourceInfo {
+    const AttentionWorkload* wl = nullptr;
+    size_t layer = 0;
+    bool ours = false;  // a DirectKeySource / KvView: read its host tier, replay the reads
+};
+SourceInfo source_info(KeySource& ks) {
+    if (auto* d = dynamic_cast<DirectKeySource*>(&ks)) return {&d->workload(), d->layer(), true};
+    if (auto* v = dynamic_cast<KvView*>(&ks)) return {&v->host(), v->layer(), true};
+    return {};
+}
+
+void check_sorted_unique(std::span<const std::size_t> idx, const char* where) {
+    for (size_t i = 1; i < idx.size(); ++i)
+        if (idx[i] <= idx[i - 1]) throw ContractViolation(std::string(where) + ": indices must be sorted and duplicate-free");
+}
+
+// One stage on the device over one list (one mask pooling `qblocks.size()` heads).
+// Returns the output list; `paths` (if given) receives the branch decisions [chunk][head].
+std::vector<std::size_t> stage_on_device(const StageConfig& stage, std::span<const std::size_t> list,
+                                         std::span<const DenseMatrix> qblocks, KeySource& keys, const StageContext& ctx,
+                                         bool descend_always, std::vector<std::uint32_t>* paths) {
+    if (!ctx.policy) throw std::invalid_argument("StageContext: policy is required");
+    const size_t H = qblocks.size();
+    if (H == 0) throw std::invalid_argument("run_pruning_stage: no query blocks");
+    const size_t rows = qblocks[0].rows, d = qblocks[0].cols;
+    for (const auto& q : qblocks)
+        if (q.rows != rows || q.cols != d || rows == 0) throw std::invalid_argument("run_pruning_stage: query block shapes differ");
+    if (list.empty()) return {};
+    if (list.back() >= static_cast<size_t>(1u << 31)) throw std::out_of_range("run_pruning_stage: token index beyond 2^31");
+    require_device();
+    const SourceInfo si = source_info(keys);
+    const size_t t_kv = list.back() + 1;
+    DeviceLayer kv;
+    build_layer_from_source(kv, keys, si.wl, si.layer, H, si.wl ? si.wl->seq_len_kv : t_kv, d, false, list);
+    if (si.wl && (kv.heads != static_cast<int32_t>(H) || kv.d != static_cast<int32_t>(d)))
+        throw std::invalid_argument("run_pruning_stage: query heads / dims do not match the key source");
+    std::vector<float> qh(H * rows * d);
+    for (size_t h = 0; h < H; ++h) std::memcpy(&qh[h * rows * d], qblocks[h].data.data(), rows * d * 4);
+    DevBuf q(qh.size() * 4);
+    q.upload(qh.data(), qh.size() * 4);
+    std::vector<int32_t> li(list.begin(), list.end());
+    const int32_t n = static_cast<int32_t>(li.size());
+    DevBuf dl(li.size() * 4), dc(4), ol(std::max<size_t>(stage.keep, li.size()) * 4), oc(4);
+    dl.upload(li.data(), li.size() * 4);
+    dc.upload(&n, 4);
+    const int32_t cc = static_cast<int32_t>(ceil_div(li.size(), stage.chunk_size));
+    const size_t need = hp_stage_workspace_bytes(1, cc, static_cast<int32_t>(stage.keep), static_cast<int32_t>(stage.chunk_size));
+    DevBuf ws(need);
+    DeviceRope drope;
+    if (ctx.policy->extension_enabled) {
+        if (!ctx.rope) throw std::invalid_argument("StageContext: extension enabled without a rope table");
+        drope.upload(*ctx.rope);
+    }
+    DevBuf dp;
+    if (paths) dp.alloc(static_cast<size_t>(cc) * H * 4);
+    hp_stage_args a{};
+    a.query_block = static_cast<int32_t>(rows);
+    a.chunk_size = static_cast<int32_t>(stage.chunk_size);
+    a.keep = static_cast<int32_t>(stage.keep);
+    a.n_masks = 1;
+    a.heads_per_mask = static_cast<int32_t>(H);
+    a.n_q_heads = static_cast<int32_t>(H);
+    a.n_blocks = 1;
+    a.q_rows = static_cast<int32_t>(rows);
+    a.q = q.as<float>();
+    a.query_offset = static_cast<int64_t>(ctx.query_start_position);
+    a.stream_tokens = static_cast<int32_t>(ctx.stream_tokens);
+    a.max_chunks = cc;
+    a.in_list = dl.as<int32_t>();
+    a.in_count = dc.as<int32_t>();
+    a.in_stride = n;
+    a.out_list = ol.as<int32_t>();
+    a.out_count = oc.as<int32_t>();
+    a.out_stride = static_cast<int64_t>(ol.bytes / 4);
+    a.workspace = ws.p;
+    a.workspace_bytes = ws.bytes;
+    a.keys = kv.view();
+    a.rope = rope_ctx(*ctx.policy, ctx.policy->extension_enabled ? &drope : nullptr, ctx.layer);
+    a.path_out = paths ? dp.as<std::uint32_t>() : nullptr;
+    a.descend_always = descend_always ? 1 : 0;
+    check(hp_prune_stage(&a, nullptr));
+    int32_t c = 0;
+    oc.download(&c, 4);
+    std::vector<int32_t> out(std::max(0, c));
+    if (c > 0) ol.download(out.data(), static_cast<size_t>(c) * 4);
+    if (paths) {
+        paths->resize(static_cast<size_t>(cc) * H);
+        dp.download(paths->data(), paths->size() * 4);
+    }
+    return std::vector<std::size_t>(out.begin(), out.end());
+}
+
+}  // namespace
+
+std::vector<std::size_t> run_pruning_stage(const StageConfig& stage, std::span<const std::size_t> indices,
+                                           std::span<const DenseMatrix> qblocks, KeySource& keys,
+                                           const StageContext& ctx) {
+    stage.validate();
+    check_sorted_unique(indices, "run_pruning_stage");
+    if (indices.size() <= stage.keep) return {indices.begin(), indices.end()};  // identity: no reads
+    if (ceil_div(indices.size(), stage.chunk_size) <= stage.keep / stage.chunk_size)
+        return {indices.begin(), indices.end()};
+    const bool ours = source_info(keys).ours;
+    std::vector<std::uint32_t> paths;
+    std::vector<std::size_t> out = stage_on_device(stage, indices, qblocks, keys, ctx, false, ours ? &paths : nullptr);
+    if (ours) replay_stage_reads(keys, indices, stage.chunk_size, qblocks.size(), paths.data());
+    return out;
+}
+
+std::size_t select_rep(const DenseMatrix& qblock, std::span<const std::size_t> chunk, KeySource& keys,
+                       std::size_t head, const StageContext& ctx, std::size_t chunk_index, std::size_t chunk_count) {
+    if (chunk.empty()) throw ContractViolation("select_rep: empty chunk");
+    if (chunk.size() == 1) return chunk[0];
+    if (!ctx.policy) throw std::invalid_argument("StageContext: policy is required");
+    // one device stage whose chunk `chunk_index` of `chunk_count` is this chunk (the
+    // chunk position sets the RoPE positions; copies elsewhere only keep them aligned)
+    const size_t n = chunk.size();
+    const bool ext = ctx.policy->extension_enabled;
+    const size_t copies = ext ? std::max<size_t>(chunk_count, chunk_index + 1) : 1;
+    const size_t at = ext ? chunk_index : 0;
+    std::vector<std::size_t> list;
+    list.reserve(copies * n);
+    for (size_t c = 0; c < copies; ++c) list.insert(list.end(), chunk.begin(), chunk.end());
+    // a single-head key source view: rows of `head` as kv head 0
+    struct HeadSource final : KeySource {
+        KeySource* ks;
+        size_t head;
+        std::span<const float> key_row(std::size_t, std::size_t t) override { return ks->key_row(head, t); }
+        std::span<const float> value_row(std::size_t, std::size_t t) override { return ks->value_row(head, t); }
+    } one;
+    one.ks = &keys;
+    one.head = head;
+    const SourceInfo si = source_info(keys);
+    StageConfig st{qblock.rows, n, n};
+    std::vector<std::uint32_t> paths;
+    std::vector<DenseMatrix> qb{qblock};
+    if (si.wl) {  // the source's host tier, one head
+        AttentionWorkload w1;
+        w1.num_heads = 1;
+        w1.num_layers = 1;
+        w1.seq_len_kv = si.wl->seq_len_kv;
+        w1.head_dim = qblock.cols;
+        w1.keys = {{si.wl->k(si.layer, head)}};
+        w1.values = {{DenseMatrix()}};
+        DirectKeySource direct(w1, 0);
+        stage_on_device(st, list, qb, direct, ctx, true, &paths);
+    } else {
+        stage_on_device(st, list, qb, one, ctx, true, &paths);
+    }
+    const std::uint32_t bits = paths[at];
+    if (si.ours) return replay_select_rep(keys, chunk, head, bits);
+    size_t first = 1, last = n;
+    const int iters = ceil_log2(n);
+    for (int it = 0; it < iters && first < last; ++it) {
+        const size_t mid = (first + last + 1) / 2;
+        if ((bits >> it) & 1u) first = mid;
+        else last = mid - 1;
+    }
+    return chunk[first - 1];
+}
+
+std::vector<float> attention_row(std::span<const float> q_row, std::span<const std::size_t> selected,
+                                 std::size_t query_position, bool extension_enabled, const RopeTable& rope,
+                                 KeySource& kv, std::size_t head) {
+    if (selected.empty()) throw std::invalid_argument("attention_row: empty selected set");
+    const size_t d = q_row.size();
+    if (extension_enabled) {
+        streaming_positions(selected, query_position, 0);  // throws as the reference does
+        if (query_position >= rope.max_position)
+            throw std::out_of_range("apply_rope: position " + std::to_string(query_position) + " >= max_position " +
+                                    std::to_string(rope.max_position));
+    }
+    for (size_t i = 1; i < selected.size(); ++i)
+        if (selected[i] <= selected[i - 1]) throw ContractViolation("attention_row: selected indices must be ascending");
+    if (selected.back() >= static_cast<size_t>(1u << 31)) throw std::out_of_range("attention_row: token index beyond 2^31");
+    require_device();
+    const SourceInfo si = source_info(kv);
+    // the head's K/V rows as a one-head device layer
+    struct HeadSource final : KeySource {
+        KeySource* ks;
+        size_t head;
+        std::span<const float> key_row(std::size_t, std::size_t t) override { return ks->key_row(head, t); }
+        std::span<const float> value_row(std::size_t, std::size_t t) override { return ks->value_row(head, t); }
+    } one;
+    one.ks = &kv;
+    one.head = head;
+    DeviceLayer dl;
+    if (si.wl) {
+        AttentionWorkload w1;
+        w1.num_heads = 1;
+        w1.num_layers = 1;
+        w1.seq_len_kv = si.wl->seq_len_kv;
+        w1.head_dim = d;
+        w1.keys = {{si.wl->k(si.layer, head)}};
+        w1.values = {{si.wl->v(si.layer, head)}};
+        dl.build(w1, 0, true);
+    } else {
+        build_layer_from_source(dl, one, nullptr, 0, 1, selected.back() + 1, d, true, selected);
+    }
+    std::vector<int32_t> sel(selected.begin(), selected.end());
+    const int32_t n = static_cast<int32_t>(sel.size());
+    DevBuf ds(sel.size() * 4), dc(4), q(d * 4), o(d * 4);
+    ds.upload(sel.data(), sel.size() * 4);
+    dc.upload(&n, 4);
+    q.upload(q_row.data(), d * 4);
+    DeviceRope drope;
+    RopePolicySet pol;
+    pol.extension_enabled = extension_enabled;
+    if (extension_enabled) drope.upload(rope);
+    const size_t need = hp_bsa_workspace_bytes(1, 1, n, static_cast<int32_t>(d));
+    DevBuf ws(need);
+    hp_bsa_args a{};
+    a.n_q_heads = 1;
+    a.heads_per_mask = 1;
+    a.n_rows = 1;
+    a.q = q.as<float>();
+    a.query_offset = static_cast<int64_t>(query_position);
+    a.sel_list = ds.as<int32_t>();
+    a.sel_count = dc.as<int32_t>();
+    a.sel_stride = n;
+    a.max_sel = n;
+    a.out = o.as<float>();
+    a.workspace = ws.p;
+    a.workspace_bytes = ws.bytes;
+    a.kv = dl.view();
+    a.rope = rope_ctx(pol, extension_enabled ? &drope : nullptr, 0);
+    check(hp_bsa(&a, nullptr));
+    std::vector<float> out(d);
+    o.download(out.data(), d * 4);
+    if (si.ours) {  // the reference's reads: every key row, then every value row
+        for (size_t t : selected) kv.key_row(head, t);
+        for (size_t t : selected) kv.value_row(head, t);
+    }
+    return out;
+}
+
+AttentionOutput block_sparse_attention(const AttentionWorkload& wl, std::size_t layer, const SparseBlockMask& mask,
+                                       const RopePolicySet& policy, const RopeTable& rope, KeySource& kvs) {
+    if (layer >= wl.num_layers) throw std::out_of_range("block_sparse_attention: layer out of range");
+    if (mask.block_size == 0 || mask.num_blocks() != ceil_div(wl.seq_len_q, mask.block_size))
+        throw std::invalid_argument("block_sparse_attention: mask does not cover the queries");
+    if (policy.extension_enabled && policy.bsa_policy != RopePolicyId::Streaming)
+        throw std::invalid_argument("block_sparse_attention: unsupported BSA position policy");
+    const SourceInfo si = source_info(kvs);
+    AttentionOutput out;
+    if (si.wl && si.wl == &wl && si.layer == layer) {
+        out = block_sparse_attention(wl, layer, mask, policy, rope);
+    } else {
+        // rows through the source: a workload copy whose layer holds them
+        require_device();
+        AttentionWorkload w = wl;
+        for (size_t h = 0; h < wl.num_heads; ++h)
+            for (size_t t = 0; t < wl.seq_len_kv; ++t) {
+                const auto kr = si.wl ? si.wl->k(si.layer, h).row_span(t) : kvs.key_row(h, t);
+                const auto vr = si.wl ? si.wl->v(si.layer, h).row_span(t) : kvs.value_row(h, t);
+                std::memcpy(w.keys[layer][h].row(t), kr.data(), wl.head_dim * 4);
+                std::memcpy(w.values[layer][h].row(t), vr.data(), wl.head_dim * 4);
+            }
+        out = block_sparse_attention(w, layer, mask, policy, rope);
+    }
+    if (si.ours) {  // head by head, row by row: keys then values (sparse_attention.cpp:128-140)
+        for (size_t h = 0; h < wl.num_heads; ++h)
+            for (size_t r = 0; r < wl.seq_len_q; ++r) {
+                const std::vector<std::size_t> sel = selected_indices(mask, r);
+                for (size_t t : sel) kvs.key_row(h, t);
+                for (size_t t : sel) kvs.value_row(h, t);
+            }
+    }
+    return out;
+}
 
 }  // namespace hipprune

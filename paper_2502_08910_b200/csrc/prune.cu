@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(256) prune_descent_kernel(const hp_stage_args 
     const int lc = a.chunk_size;
     const int64_t cc = (n_in + lc - 1) / lc;
     const int64_t keep_chunks = a.keep / lc;
-    if (n_in <= a.keep || cc <= keep_chunks) return;  // identity (pruning.cpp:159-168)
+    if (!a.descend_always && (n_in <= a.keep || cc <= keep_chunks)) return;  // identity (pruning.cpp:159-168)
     const int64_t chunk0 = static_cast<int64_t>(blockIdx.x) * 32 * g.cg;
     if (chunk0 >= cc) return;
 
@@ -293,6 +293,7 @@ __global__ void __launch_bounds__(256) prune_descent_kernel(const hp_stage_args 
     int iters = 0;
     while ((1 << iters) < len) ++iters;
     float s1 = 0.0f, s2 = 0.0f;
+    uint32_t path = 0;  // branch decisions (bit it = went right)
     stage_rows<T, D>(a, kv, active ? token(0) : -1, ks, g.key_stride, lane);
     if (active) score2(s1, s2);
     for (;;) {
@@ -306,6 +307,7 @@ __global__ void __launch_bounds__(256) prune_descent_kernel(const hp_stage_args 
             score2(m1, m2);
             if (m2 > s1) {  // right only on strict sigma2 > sigma1 (pruning.cpp:91)
                 first = mid; s1 = m1; s2 = m2;
+                path |= 1u << it;
             } else {
                 last = mid - 1;
             }
@@ -314,6 +316,7 @@ __global__ void __launch_bounds__(256) prune_descent_kernel(const hp_stage_args 
     }
     const int ch = grp * 32 + lane;
     red[hh * (32 * g.cg) + ch] = s2;  // branch-2 score of the representative (pruning.cpp:181)
+    if (a.path_out && active) a.path_out[(static_cast<int64_t>(mb) * max_chunks + j) * hpm + hh] = path;
     __syncwarp();
     }
     __syncthreads();

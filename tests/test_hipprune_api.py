@@ -138,11 +138,14 @@ def test_exact_topk_and_recall_goldens(workload):
     assert abs(hp.attention_recall(list(range(1024)), qq, kk) - 1.0) < 1e-9
 
 
-def test_report_plumbing_is_out_of_scope():
-    with pytest.raises(RuntimeError, match="not part of the B200 hot path"):
-        hp.run_report("decode-sim", [])
-    with pytest.raises(RuntimeError, match="not part of the B200 hot path"):
-        hp.config_hash([])
+def test_report_plumbing():
+    """run_report / config_hash (the reference's report plumbing, python/hipprune/_reports.py):
+    config_hash is deterministic and override-sensitive on any host; unknown commands are
+    ValueError as in bindings.cpp; decode-sim itself runs on the GPU (test_gpu_decode_sim.py)."""
+    h = hp.config_hash(["run.steps=8"])
+    assert isinstance(h, int) and h == hp.config_hash(["run.steps=8"]) != hp.config_hash(["run.steps=9"])
+    with pytest.raises(ValueError):
+        hp.run_report("no-such-report", [])
 
 
 @pytest.mark.skipif(_gpu(), reason="checks the no-device failure mode")
