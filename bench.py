@@ -145,6 +145,19 @@ def cpu_reference_step(q, k, v, threads):
     return secs, kind
 
 
+def host_cpu() -> dict:
+    """The host the CPU baseline ran on: CPU model and logical core count."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
 def host_workload(t, layer=0):
     """The same synthetic Q/K/V as the GPU arm's layer `layer` (per (layer, group) seeds),
     as host fp32 (bf16-rounded)."""
@@ -181,7 +194,8 @@ def run_reference(args, rank, world):
             "data": "synthetic (reference generator recipe, torch RNG), bf16-rounded values in fp32",
             "config": config(args, 1),
             "cpu_baseline": {"value": us, "unit": "us/layer", "cores": threads, "kind": kind,
-                             "sample": f"full layer step, {GROUPS} KV groups x {HPM} q-heads at T={args.ctx}"},
+                             "sample": f"full layer step, {GROUPS} KV groups x {HPM} q-heads at T={args.ctx}",
+                             **host_cpu()},
             "e2e": {"value": us, "unit": "us/layer", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -421,7 +435,8 @@ def main():
                 secs, kind = cpu_reference_step(qh, kh, vh, threads)
                 reps.append(secs)
             cpu = {"value": 1e6 * min(reps), "unit": "us/layer", "cores": threads, "kind": kind,
-                   "sample": f"one full-refresh layer step ({GROUPS} KV groups x {HPM} q-heads, T={t}), best of 2"}
+                   "sample": f"one full-refresh layer step ({GROUPS} KV groups x {HPM} q-heads, T={t}), best of 2",
+                   **host_cpu()}
             del kh, vh
         except Exception as e:  # the CPU baseline is informational
             cpu = {"value": None, "unit": "us/layer", "cores": None, "kind": None, "sample": f"failed: {e}"}

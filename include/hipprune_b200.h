@@ -214,9 +214,6 @@ typedef struct hp_bsa_prefill_args {
 } hp_bsa_prefill_args;
 
 size_t hp_bsa_prefill_smem_bytes(int32_t max_union);
-/* Developer instrumentation: the prefill kernel's thread 0 writes progress codes to
- * this (device-mapped pinned host) word; NULL disables. */
-int hp_debug_prefill_progress(int* mapped_word);
 int hp_bsa_prefill(const hp_bsa_prefill_args* args, void* stream);
 
 /* ------------------------------------------------------------------------ *
@@ -398,13 +395,6 @@ int hp_decode_materialize(const hp_list_ref* refs, const int32_t* const* counts,
                           int32_t* const* outs, const int64_t* out_strides, int32_t n_lists,
                           int32_t n_masks, int32_t max_count, void* stream);
 
-/* Developer instrumentation: per-CTA %globaltimer / clock64 stamps of the fused decode
- * kernels (kernel_id 10 + l_c = stage descent, 3 = top-k, 2 = BSA) into
- * buf [16384][8] u64 (first 8192 rows: timer, next 8192: clock). NULL disables. */
-int hp_trace_enable(unsigned long long* buf, int kernel_id);
-/* Developer instrumentation (dev build only, no-op otherwise): kernel `kernel_id` returns
- * early at its cut point `at` (-1 disables), to time a kernel prefix in isolation. */
-int hp_debug_cut(int kernel_id, int at);
 
 /* ------------------------------------------------------------------------ *
  * On-GPU LRU page cache over a pinned host tier (replaces TieredKvStore::

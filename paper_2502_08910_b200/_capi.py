@@ -139,9 +139,9 @@ EXPORTS = ["hp_last_error", "hp_version", "hp_device_available", "hp_build_rope_
            "hp_selected_indices", "hp_bsa_workspace_bytes", "hp_bsa", "hp_lse_merge",
            "hp_decode_stage_workspace_bytes", "hp_decode_stage", "hp_decode_bsa_workspace_bytes",
            "hp_decode_bsa", "hp_decode_stage_variant", "hp_decode_bsa_variant",
-           "hp_decode_layer_workspace_bytes", "hp_decode_layer_supported", "hp_decode_layer", "hp_decode_materialize", "hp_decode_append", "hp_trace_enable", "hp_debug_cut",
+           "hp_decode_layer_workspace_bytes", "hp_decode_layer_supported", "hp_decode_layer", "hp_decode_materialize", "hp_decode_append",
            "hp_cache_workspace_bytes", "hp_cache_commit", "hp_select_topk", "hp_select_topk_sharded",
-           "hp_bsa_prefill_smem_bytes", "hp_bsa_prefill", "hp_debug_prefill_progress"]
+           "hp_bsa_prefill_smem_bytes", "hp_bsa_prefill"]
 
 
 def lib():
@@ -192,8 +192,9 @@ def lib():
     L.hp_decode_layer_supported.argtypes = [C.POINTER(DecodeLayerArgs)]
     L.hp_decode_layer.restype = C.c_int
     L.hp_decode_layer.argtypes = [C.POINTER(DecodeLayerArgs), C.c_void_p]
-    L.hp_decode_layer_cluster.restype = C.c_int
-    L.hp_decode_layer_cluster.argtypes = [C.c_int]
+    if hasattr(L, "hp_decode_layer_cluster"):  # dev builds only (include/hipprune_b200_dev.h)
+        L.hp_decode_layer_cluster.restype = C.c_int
+        L.hp_decode_layer_cluster.argtypes = [C.c_int]
     L.hp_decode_materialize.restype = C.c_int
     L.hp_decode_materialize.argtypes = [C.POINTER(ListRef), C.POINTER(C.c_void_p),
                                         C.POINTER(C.c_void_p), C.POINTER(C.c_int64), C.c_int32,

@@ -45,7 +45,7 @@ def build_cuda(force: bool = False, verbose: bool = False) -> Path:
     variant = os.environ.get("HP_VARIANT")
     if variant:
         out = LIB / f"libhipprune_b200_{variant}.so"
-        dev_flags = dev_flags + os.environ.get("HP_VARIANT_FLAGS", "").split()
+        dev_flags = dev_flags + ["-DHP_DEV"] + os.environ.get("HP_VARIANT_FLAGS", "").split()
     deps = [CSRC / s for s in CUDA_SOURCES] + list(CSRC.glob("*.cuh")) + [ROOT / "include" / "hipprune_b200.h"]
     if not force and not _stale(out, deps):
         return out

@@ -1373,6 +1373,7 @@ int bsa_keys_per_cta(int64_t max_sel, int groups) {
 
 // Developer instrumentation: record per-CTA phase stamps of kernel `kernel_id`
 // (1 = decode stage, 2 = decode BSA) into buf [n_cta][8] (NULL disables).
+#if defined(HP_TRACE) || defined(HP_DEV)  // developer hooks: dev builds only (include/hipprune_b200_dev.h)
 extern "C" int hp_debug_cut(int kernel_id, int at) {
     if (int rc = hph::check_cuda(cudaMemcpyToSymbol(g_cut_kernel, &kernel_id, sizeof(int)), "hp_debug_cut")) return rc;
     return hph::check_cuda(cudaMemcpyToSymbol(g_cut_at, &at, sizeof(int)), "hp_debug_cut");
@@ -1382,6 +1383,7 @@ extern "C" int hp_trace_enable(unsigned long long* buf, int kernel_id) {
     if (int rc = hph::check_cuda(cudaMemcpyToSymbol(g_trace_buf, &buf, sizeof(buf)), "hp_trace_enable")) return rc;
     return hph::check_cuda(cudaMemcpyToSymbol(g_trace_kernel, &kernel_id, sizeof(int)), "hp_trace_enable");
 }
+#endif
 
 // tickets, then chunk scores with room for up to kWideHeadPlanes per-head planes (the
 // one-wave kernel keeps every head's representative score; the selection maxes them)

@@ -731,6 +731,7 @@ extern "C" int hp_decode_layer_supported(const hp_decode_layer_args* ap) {
     return 1;
 }
 
+#if defined(HP_TRACE) || defined(HP_DEV)  // developer hooks: dev builds only (include/hipprune_b200_dev.h)
 // dev build: per-CTA phase stamps of the layer kernel (trace id 20) into buf
 extern "C" int hp_layer_trace_enable(unsigned long long* buf, int kernel_id) {
     if (int rc = hph::check_cuda(cudaMemcpyToSymbol(g_trace_buf, &buf, sizeof(buf)), "hp_layer_trace_enable")) return rc;
@@ -742,6 +743,7 @@ extern "C" int hp_decode_layer_cluster(int cs) {
     g_cluster_override = cs;  // <= 0: grid mode
     return HP_OK;
 }
+#endif
 
 extern "C" int hp_decode_layer(const hp_decode_layer_args* ap, void* stream) {
     if (!ap) return hph::set_error(HP_INVALID_ARGUMENT, "hp_decode_layer: null args");

@@ -445,9 +445,11 @@ __global__ void __launch_bounds__(kThreads, 1) bsa_prefill_tc_kernel(const hp_bs
 
 }  // namespace
 
+#if defined(HP_TRACE) || defined(HP_DEV)  // developer hook: dev builds only (include/hipprune_b200_dev.h)
 extern "C" int hp_debug_prefill_progress(int* mapped_word) {
     return hph::check_cuda(cudaMemcpyToSymbol(g_pf_progress, &mapped_word, sizeof(mapped_word)), "hp_debug_prefill_progress");
 }
+#endif
 
 extern "C" size_t hp_bsa_prefill_smem_bytes(int32_t max_union) {
     // union list padded to whole 128-key tiles: the selection test reads it 16 bytes at a time

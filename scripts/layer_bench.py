@@ -9,7 +9,7 @@ from paper_2502_08910_b200 import device as D, synth
 from paper_2502_08910_b200._capi import lib
 
 t = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 20
-css = [int(x) for x in sys.argv[2].split(",")] if len(sys.argv) > 2 else [0, 8]
+css = [int(x) for x in sys.argv[2].split(",")] if len(sys.argv) > 2 else [0]  # cluster sizes need a dev build (HP_VARIANT)
 groups, hpm, d = 8, 4, 128
 stages = [(64, 256, 32768), (64, 32, 8192), (64, 8, 2048)]
 q, k, v = synth.generate(groups * hpm, groups, t, d, seed=1)
@@ -51,7 +51,8 @@ print("per-stage  " + "  ".join(f"{n} {v:7.2f}" for n, v in ref.items()), flush=
 m_ref = [c.clone() for c in layer.cache]
 layer._fused = "always"
 for cs in css:
-    lib().hp_decode_layer_cluster(cs)
+    if hasattr(lib(), "hp_decode_layer_cluster"):
+        lib().hp_decode_layer_cluster(cs)
     layer.run(t); torch.cuda.synchronize()
     same = all(torch.equal(a, b) for a, b in zip(m_ref, layer.cache))
     res = {n: timeit(lambda fl=fl: layer.run(t, refresh=fl, materialize=False)) for n, fl in pats.items()}

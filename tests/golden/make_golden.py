@@ -25,8 +25,19 @@ sys.path.insert(0, str(HERE.parents[1]))
 from oracle import Oracle, build  # noqa: E402
 
 
+def hipw() -> None:
+    """A reference-written HIPW dump + its checksum (workload.cpp:222-312), for the
+    interchange test (tests/test_hipprune_api.py::test_reads_reference_written_dump)."""
+    import subprocess
+    path = HERE / "ref_small.hipw"
+    res = subprocess.run([str(HERE.parents[1] / "oracle" / "_ref" / "ref_hipw"), str(path), "2", "2", "64", "16",
+                          "8", "21"], check=True, capture_output=True, text=True)
+    (HERE / "ref_small.crc").write_text(res.stdout.strip() + "\n")
+
+
 def main() -> None:
     build("all")
+    hipw()
     R = Oracle("reference")
     out = {}
     # 1. build_mask on reference-generated workloads (test_pruning.cpp:323-349 plan, 3k plan)

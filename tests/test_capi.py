@@ -85,3 +85,15 @@ def test_device_probe_reports_no_device_here(capi):
     from paper_2502_08910_b200 import device as D
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         D.require_cuda()
+
+
+def test_product_library_has_no_dev_hooks():
+    """The developer hooks (include/hipprune_b200_dev.h) exist only in dev builds."""
+    import ctypes
+    from paper_2502_08910_b200 import _capi
+    if not _capi.LIB_PATH.exists() or "trace" in _capi.LIB_PATH.name or "HP_LIB" in __import__("os").environ:
+        pytest.skip("product library not built / a dev build is selected")
+    L = ctypes.CDLL(str(_capi.LIB_PATH))
+    for name in ("hp_trace_enable", "hp_layer_trace_enable", "hp_debug_cut", "hp_debug_prefill_progress",
+                 "hp_decode_layer_cluster"):
+        assert not hasattr(L, name), name

@@ -269,3 +269,23 @@ def test_cache_disabled_equivalence_acceptance7():
         for i in range(3):
             refreshes[i] += bool(tel["refreshed"][i])
     assert refreshes == [3, 6, 12]
+
+
+def test_reads_reference_written_dump(tmp_path):
+    """HIPW interchange (workload.cpp:222-312): a dump the unmodified reference wrote
+    (tests/golden/ref_small.hipw, tests/golden/make_golden.py) loads here with the same
+    tensors as this library's generator (bit-identical), the same dump_checksum, and
+    re-saving it reproduces the file byte for byte."""
+    from pathlib import Path
+    gold = Path(__file__).resolve().parent / "golden"
+    w = hp.load_dump(str(gold / "ref_small.hipw"))
+    assert (w.num_heads, w.num_layers, w.seq_len_kv, w.seq_len_q, w.head_dim) == (2, 2, 64, 16, 8)
+    assert hp.dump_checksum(w) == int((gold / "ref_small.crc").read_text())
+    mine = hp.generate(heads=2, layers=2, seq_kv=64, seq_q=16, dim=8, seed=21)
+    for l in range(2):
+        for h in range(2):
+            assert np.array_equal(w.q(l, h), mine.q(l, h)) and np.array_equal(w.k(l, h), mine.k(l, h))
+            assert np.array_equal(w.v(l, h), mine.v(l, h))
+    out = tmp_path / "again.hipw"
+    hp.save_dump(w, str(out))
+    assert out.read_bytes() == (gold / "ref_small.hipw").read_bytes()
