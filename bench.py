@@ -57,6 +57,7 @@ def parse():
     p.add_argument("--layers", type=int, default=8,
                    help="layers per decode step (distinct KV each); value = step time / layers")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-ext", action="store_true", help="skip the RoPE-extension step (ext_on_us)")
     p.add_argument("--shard-of", type=int, default=0,
                    help="dev: run as rank 0 of an N-way KV-group split in ONE process (no process "
                         "group) to measure one GPU's share of the N-GPU step")
@@ -337,6 +338,41 @@ def main():
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         mean_step, amort_us, bsa_us = tt.tolist()
 
+    # ---- RoPE extension on (rope_policy.cpp; relative pruning positions past layer 3 and
+    # streaming positions in the BSA): the same full-refresh step through the rotating kernels
+    ext_us = None
+    if not args.no_ext:
+        rope = D_.RopeTable(t + 2, D, device=dev)
+        ext_layers = [D_.FusedDecodeLayer(ly.kv, STAGES, sink=SINK, stream_tokens=STREAM, n_q_heads=ly.n_q_heads,
+                                          n_masks=ly.n_masks, policy=D_.RopePolicy(extension=True), rope=rope,
+                                          device=dev) for ly in layers]
+        for el, ly in zip(ext_layers, layers):
+            el.q.copy_(ly.q)
+            el.run(t)
+        torch.cuda.synchronize()
+        eg = torch.cuda.CUDAGraph()
+        stream.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.graph(eg, stream=stream):
+            side.wait_stream(stream)
+            for el in ext_layers:
+                el.run(t, mat_stream=side)
+            stream.wait_stream(side)
+        et = []
+        for i in range(max(3, args.steps // 2)):
+            do_flush()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(cur)
+            eg.replay()
+            b.record(cur)
+            et.append((a, b))
+        torch.cuda.synchronize()
+        ext_us = statistics.mean(1000.0 * a.elapsed_time(b) / L for a, b in et)
+        if world > 1:
+            tt = torch.tensor([ext_us], dtype=torch.float64, device=dev)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            ext_us = tt.item()
+        del ext_layers, rope, eg
+
     # ---- dominant kernel: the stage-1 descent (decode_stage_kernel), timed alone on its
     # stream: a graph of its L per-layer launches, L2 flushed before each replay
     s1_graph = torch.cuda.CUDAGraph()
@@ -454,6 +490,8 @@ def main():
             "amortized_us": amort_us,
             "amortized_schedule": "refresh (16, 8, 4), averaged over whole cycles",
             "bsa_only_us": bsa_us, "allgather_us": allgather_us,
+            "ext_on_us": ext_us, "ext_on_note": "full-refresh step with RoPE extension on (layer 4: relative "
+                                                "pruning positions, two rotated dots per key row; streaming BSA)",
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": f"stage-1 descent ({layers[0].dispatch()[0] if layers[0].dispatch()[0] else 'stage 1'} kernel, {ng} KV groups)",

@@ -146,13 +146,14 @@ decode_stage_kernel(const hp_decode_stage_args a, float* scores, int* tickets, i
         };
         const float* cs1 = nullptr; const float* sn1 = nullptr;
         const float* cs2 = nullptr; const float* sn2 = nullptr;
-        bool same_rot = true;
+        bool same_rot = true, plain1 = false;
         if constexpr (EXT) {
             constexpr int half = kD / 2;
             const int64_t p1 = rope_k_position(a.rope, 1, j), p2 = rope_k_position(a.rope, 2, j);
             cs1 = a.rope.cos_tab + p1 * half; sn1 = a.rope.sin_tab + p1 * half;
             cs2 = a.rope.cos_tab + p2 * half; sn2 = a.rope.sin_tab + p2 * half;
             same_rot = p1 == p2;
+        plain1 = p1 == 0;
         }
         int first = 1, last = len, it = 0, iters = 0;
         while ((1 << iters) < len) ++iters;
@@ -162,10 +163,16 @@ decode_stage_kernel(const hp_decode_stage_args a, float* scores, int* tickets, i
         stage_rows<T>(a.keys, kvh, active ? token(0) : -1, wstage, lane,
                       prefetch && active && iters > 0 ? token(mid0 - 1) : -1);
         if (k == 0) trace(10 + lc, 3);
-        if (active) {
-            s1 = score(cs1, sn1);
-            s2 = same_rot ? s1 : score(cs2, sn2);
-        }
+        // both branches' scores of the staged row (one pass for bf16 rows with RoPE)
+        auto score2 = [&](float& b1, float& b2) {
+            if constexpr (EXT && sizeof(T) == 2) {
+                dot_row_rot2_bf16(myrow, swz, qrow, cs1, sn1, cs2, sn2, same_rot, b1, b2, plain1);
+            } else {
+                b1 = score(cs1, sn1);
+                b2 = same_rot ? b1 : score(cs2, sn2);
+            }
+        };
+        if (active) score2(s1, s2);
         if (k == 0) trace(10 + lc, 4);
         for (;;) {
             const bool go = active && it < iters && first < last;
@@ -180,8 +187,8 @@ decode_stage_kernel(const hp_decode_stage_args a, float* scores, int* tickets, i
             stage_rows<T>(a.keys, kvh, go ? token(mid - 1) : -1, wstage, lane, pf_r, pf_l);
             if (k == 0 && it == 0) trace(10 + lc, 5);
             if (go) {
-                const float m1 = score(cs1, sn1);
-                const float m2 = same_rot ? m1 : score(cs2, sn2);
+                float m1, m2;
+                score2(m1, m2);
                 if (m2 > s1) { first = mid; s1 = m1; s2 = m2; } else { last = mid - 1; }
                 ++it;
             }
@@ -440,7 +447,11 @@ decode_stage_look_kernel(const hp_decode_stage_args a, float* scores, int cg, in
 // over heads in head order, as the reference does.
 constexpr int kWideWarps = 7;
 
-template <typename T>
+// EXT (RoPE extension, rope_policy.cpp:18-72): each warp rotates its head's q once into
+// its own 512 B of shared memory (rotate_queries, pruning.cpp:39-52) and every staged
+// key row is rotated element by element inside the sequential dot at the chunk's
+// branch-1 / branch-2 key positions (separately rounded, as apply_rope_inplace).
+template <typename T, bool EXT = false>
 __global__ void __launch_bounds__(kWideWarps * 32, 4)
 decode_stage_wide_kernel(const hp_decode_stage_args a, float* hscores, int groups) {
     pdl_trigger();
@@ -479,6 +490,26 @@ decode_stage_wide_kernel(const hp_decode_stage_args a, float* hscores, int group
         if (len > 1) contiguous = ref_token(a.in, m, base + len - 1) - t_first == len - 1;
     }
     auto token = [&](int i) -> int64_t { return contiguous ? t_first + i : ref_token(a.in, m, base + i); };
+    float* qrot = reinterpret_cast<float*>(smem + static_cast<size_t>(kWideWarps) * 32 * G::stride) + w * kD;
+    const float* cs1 = nullptr; const float* sn1 = nullptr;
+    const float* cs2 = nullptr; const float* sn2 = nullptr;
+    bool same_rot = true, plain1 = false;
+    if constexpr (EXT) {
+        constexpr int half = kD / 2;
+        const int64_t qp = rope_q_position(a.rope, a.query_position, a.stream_tokens, cc);
+        for (int e = lane; e < half; e += 32) {
+            const float x = __ldg(qrow + e), y = __ldg(qrow + e + half);
+            const float c = a.rope.cos_tab[qp * half + e], sn = a.rope.sin_tab[qp * half + e];
+            qrot[e] = __fsub_rn(__fmul_rn(x, c), __fmul_rn(y, sn));
+            qrot[e + half] = __fadd_rn(__fmul_rn(x, sn), __fmul_rn(y, c));
+        }
+        __syncwarp();
+        const int64_t p1 = rope_k_position(a.rope, 1, j), p2 = rope_k_position(a.rope, 2, j);
+        cs1 = a.rope.cos_tab + p1 * half; sn1 = a.rope.sin_tab + p1 * half;
+        cs2 = a.rope.cos_tab + p2 * half; sn2 = a.rope.sin_tab + p2 * half;
+        same_rot = p1 == p2;
+        plain1 = p1 == 0;
+    }
     auto score = [&]() -> float {
         // q through L1: every lane reads the same address (one wavefront per load)
         const float4* q4 = reinterpret_cast<const float4*>(qrow);
@@ -513,9 +544,9 @@ decode_stage_wide_kernel(const hp_decode_stage_args a, float* hscores, int group
     };
     int first = 1, last = len, it = 0, iters = 0;
     while ((1 << iters) < len) ++iters;
-    float s1 = 0.f;
+    float s1 = 0.f, s2 = 0.f;
     stage_rows<T, false>(a.keys, kvh, active ? token(0) : -1, wstage, lane);
-    {
+    if constexpr (!EXT) {
         // FFMA when every product is exact (bf16-exact q, keys certified), FMUL+FADD
         // otherwise — checked while the first gather is in flight
         bool q_safe = true;
@@ -525,19 +556,32 @@ decode_stage_wide_kernel(const hp_decode_stage_args a, float* hscores, int group
     }
     cp_async_wait_all();
     __syncwarp();
-    if (active) s1 = score();
+    // branch-1 / branch-2 scores of a staged row (identical without rotation)
+    auto score2 = [&](float& b1, float& b2) {
+        if constexpr (EXT && sizeof(T) == 2) {
+            dot_row_rot2_bf16(myrow, swz, qrot, cs1, sn1, cs2, sn2, same_rot, b1, b2, plain1);
+        } else if constexpr (EXT) {
+            b1 = dot_row_rot<T>(myrow, swz, qrot, cs1, sn1);
+            b2 = same_rot ? b1 : dot_row_rot<T>(myrow, swz, qrot, cs2, sn2);
+        } else {
+            b1 = b2 = score();
+        }
+    };
+    if (active) score2(s1, s2);
     for (;;) {
         const bool go = active && it < iters && first < last;
         if (!__any_sync(0xffffffffu, go)) break;
         const int mid = (first + last + 1) >> 1;
         stage_rows<T>(a.keys, kvh, go ? token(mid - 1) : -1, wstage, lane);
         if (go) {
-            const float m2 = score();
-            if (m2 > s1) { first = mid; s1 = m2; } else { last = mid - 1; }
+            float m1, m2;
+            score2(m1, m2);
+            if (m2 > s1) { first = mid; s1 = m1; s2 = m2; } else { last = mid - 1; }  // pruning.cpp:91
             ++it;
         }
     }
-    if (active) hscores[(static_cast<int64_t>(m) * hpm + hh) * a.max_chunks + j] = s1;
+    // the representative's branch-2 score (pruning.cpp:181)
+    if (active) hscores[(static_cast<int64_t>(m) * hpm + hh) * a.max_chunks + j] = s2;
 }
 
 // ------------------------------------------------- all-rows stage kernel (small l_c)
@@ -554,7 +598,10 @@ decode_stage_wide_kernel(const hp_decode_stage_args a, float* hscores, int group
 constexpr int kAllRowsWarps = 8;
 constexpr int kAllRowsHeads = 4;  // accumulators per lane (heads per pass)
 
-template <typename T>
+// EXT: q rotated in shared memory once per CTA; each lane's row dotted rotated at its
+// chunk's branch-1 and branch-2 key positions, and the replay compares branch-2 of the
+// mid with branch-1 of the current first, as select_rep_rotated does.
+template <typename T, bool EXT = false>
 __global__ void __launch_bounds__(kAllRowsWarps * 32)
 decode_stage_allrows_kernel(const hp_decode_stage_args a, float* scores) {
     pdl_trigger();
@@ -599,10 +646,31 @@ decode_stage_allrows_kernel(const hp_decode_stage_args a, float* scores) {
         qs[i] = x;
         q_safe &= q_product_safe(x);
     }
-    const bool use_fma = __syncthreads_and(q_safe) && sizeof(T) == 2 && a.keys_exact != nullptr && *a.keys_exact != 0;
+    const bool use_fma = __syncthreads_and(q_safe) && !EXT && sizeof(T) == 2 && a.keys_exact != nullptr && *a.keys_exact != 0;
     if (use_fma) {
         for (int i = threadIdx.x; i < hpm * (kD / 2); i += blockDim.x)
             qb[i] = (__float_as_uint(qs[2 * i]) >> 16) | (__float_as_uint(qs[2 * i + 1]) & 0xffff0000u);
+    }
+    const float* cs1 = nullptr; const float* sn1 = nullptr;
+    const float* cs2 = nullptr; const float* sn2 = nullptr;
+    bool same_rot = true, plain1 = false;
+    if constexpr (EXT) {
+        constexpr int half = kD / 2;
+        const int64_t qp = rope_q_position(a.rope, a.query_position, a.stream_tokens, cc);
+        for (int i = threadIdx.x; i < hpm * half; i += blockDim.x) {
+            const int hh = i / half, e = i - hh * half;
+            float* qr = qs + hh * kD;
+            const float c = a.rope.cos_tab[qp * half + e], sn = a.rope.sin_tab[qp * half + e];
+            const float x = qr[e], y = qr[e + half];
+            qr[e] = __fsub_rn(__fmul_rn(x, c), __fmul_rn(y, sn));
+            qr[e + half] = __fadd_rn(__fmul_rn(x, sn), __fmul_rn(y, c));
+        }
+        const int64_t jj = live ? j : 0;
+        const int64_t p1 = rope_k_position(a.rope, 1, jj), p2 = rope_k_position(a.rope, 2, jj);
+        cs1 = a.rope.cos_tab + p1 * half; sn1 = a.rope.sin_tab + p1 * half;
+        cs2 = a.rope.cos_tab + p2 * half; sn2 = a.rope.sin_tab + p2 * half;
+        same_rot = p1 == p2;
+        plain1 = p1 == 0;
     }
     __syncthreads();  // unconditional (see decode_stage_kernel)
     if (cut == 1) return;
@@ -616,11 +684,22 @@ decode_stage_allrows_kernel(const hp_decode_stage_args a, float* scores) {
     while ((1 << iters) < lc) ++iters;
     float best = -INFINITY;
     for (int h0 = 0; h0 < hpm; h0 += kAllRowsHeads) {
-        float acc[kAllRowsHeads];
+        float acc[kAllRowsHeads], acc1[kAllRowsHeads];  // branch-2 / branch-1 row scores
 #pragma unroll
         for (int u = 0; u < kAllRowsHeads; ++u) acc[u] = 0.0f;
         const int nh = min(kAllRowsHeads, hpm - h0);
-        if (use_fma && nh == kAllRowsHeads) {  // full group of heads: constant q offsets, no index math
+        if constexpr (EXT) {
+#pragma unroll
+            for (int u = 0; u < kAllRowsHeads; ++u) {
+                const float* qr = qs + (h0 + min(u, nh - 1)) * kD;
+                if constexpr (sizeof(T) == 2) {
+                    dot_row_rot2_bf16(row, swz, qr, cs1, sn1, cs2, sn2, same_rot, acc1[u], acc[u], plain1);
+                } else {
+                    acc1[u] = dot_row_rot<T>(row, swz, qr, cs1, sn1);
+                    acc[u] = same_rot ? acc1[u] : dot_row_rot<T>(row, swz, qr, cs2, sn2);
+                }
+            }
+        } else if (use_fma && nh == kAllRowsHeads) {  // full group of heads: constant q offsets, no index math
             const uint4* q4 = reinterpret_cast<const uint4*>(qb + h0 * (kD / 2));
             uint4 wv[16];
 #pragma unroll
@@ -669,18 +748,34 @@ decode_stage_allrows_kernel(const hp_decode_stage_args a, float* scores) {
         // rounds for every lane: a short chunk settles early and idles.
 #pragma unroll
         for (int u = 0; u < kAllRowsHeads; ++u) {
-            const float sc = r < len ? acc[u] : -INFINITY;
-            int first = 1, last = len;
-            float s1 = __shfl_sync(0xffffffffu, sc, c0);
-            for (int it = 0; it < iters; ++it) {
-                const int mid = (first + last + 1) >> 1;
-                const bool go = first < last;
-                const float s2 = __shfl_sync(0xffffffffu, sc, c0 + (go ? mid - 1 : 0));
-                if (go) {
-                    if (s2 > s1) { first = mid; s1 = s2; } else { last = mid - 1; }
+            const float sc = r < len ? acc[u] : -INFINITY;  // branch-2 score of this lane's row
+            if constexpr (EXT) {
+                const float sc1 = r < len ? acc1[u] : -INFINITY;
+                int first = 1, last = len;
+                float s1 = __shfl_sync(0xffffffffu, sc1, c0), s2 = __shfl_sync(0xffffffffu, sc, c0);
+                for (int it = 0; it < iters; ++it) {
+                    const int mid = (first + last + 1) >> 1;
+                    const bool go = first < last;
+                    const int src = c0 + (go ? mid - 1 : 0);
+                    const float m2 = __shfl_sync(0xffffffffu, sc, src), m1 = __shfl_sync(0xffffffffu, sc1, src);
+                    if (go) {
+                        if (m2 > s1) { first = mid; s1 = m1; s2 = m2; } else { last = mid - 1; }
+                    }
                 }
+                if (u < nh) best = (best < s2) ? s2 : best;  // max over heads of branch 2 (pruning.cpp:181-182)
+            } else {
+                int first = 1, last = len;
+                float s1 = __shfl_sync(0xffffffffu, sc, c0);
+                for (int it = 0; it < iters; ++it) {
+                    const int mid = (first + last + 1) >> 1;
+                    const bool go = first < last;
+                    const float s2 = __shfl_sync(0xffffffffu, sc, c0 + (go ? mid - 1 : 0));
+                    if (go) {
+                        if (s2 > s1) { first = mid; s1 = s2; } else { last = mid - 1; }
+                    }
+                }
+                if (u < nh) best = (best < s1) ? s1 : best;  // max over heads (pruning.cpp:182)
             }
-            if (u < nh) best = (best < s1) ? s1 : best;  // max over heads (pruning.cpp:182)
         }
     }
     if (cut == 4) return;
@@ -1218,12 +1313,12 @@ int stage_variant(const hp_decode_stage_args& a, size_t elem) {
     const int hpm = a.heads_per_mask;
     const int groups = (a.max_chunks + 31) / 32;
     const int64_t wide_items = static_cast<int64_t>(a.n_masks) * groups * hpm;
-    if (!ext && a.scores_out == nullptr && a.chunk_size > 8 && hpm <= 8 &&
+    if (a.scores_out == nullptr && a.chunk_size > 8 && hpm <= 8 &&
         align_up(static_cast<size_t>(a.n_masks) * 4, 256) + static_cast<size_t>(a.n_masks) * hpm * a.max_chunks * 4 <=
             a.workspace_bytes &&
         wide_items > 2048)
         return HP_STAGE_WIDE;
-    if (!ext && a.chunk_size <= 8 && 32 % a.chunk_size == 0 && (a.n_q_heads / a.keys.n_kv) % hpm == 0)
+    if (a.chunk_size <= 8 && 32 % a.chunk_size == 0 && (a.n_q_heads / a.keys.n_kv) % hpm == 0)
         return HP_STAGE_ALLROWS;
     if (!ext && elem == 2 && kLookahead) return HP_STAGE_LOOKAHEAD;
     return HP_STAGE_CLASSIC;
@@ -1246,8 +1341,9 @@ cudaError_t launch_stage(const hp_decode_stage_args& a, float* scores, int* tick
     const int variant = stage_variant(a, sizeof(T));
     if (variant == HP_STAGE_WIDE) {
         // big stage: one wave of 7-warp CTAs, per-head scores (decode_stage_wide_kernel)
-        const size_t smem3 = static_cast<size_t>(kWideWarps) * 32 * G::stride;
-        auto k3 = decode_stage_wide_kernel<T>;
+        // + one rotated q per warp with RoPE extension (3 CTAs per SM then)
+        const size_t smem3 = static_cast<size_t>(kWideWarps) * 32 * G::stride + (EXT ? kWideWarps * kD * 4 : 0);
+        auto k3 = decode_stage_wide_kernel<T, EXT>;
         e = cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem3));
         if (e != cudaSuccess) return e;
         head_planes = hpm;
@@ -1257,7 +1353,7 @@ cudaError_t launch_stage(const hp_decode_stage_args& a, float* scores, int* tick
         // short chunks: gather every row of a chunk at once (decode_stage_allrows_kernel)
         const size_t smem2 = static_cast<size_t>(kAllRowsWarps) * 32 * G::stride + static_cast<size_t>(hpm) * kD * 6;
         const int per_cta = kAllRowsWarps * (32 / a.chunk_size);
-        auto k2 = decode_stage_allrows_kernel<T>;
+        auto k2 = decode_stage_allrows_kernel<T, EXT>;
         e = cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem2));
         if (e != cudaSuccess) return e;
         e = launch_pdl(k2, dim3((a.max_chunks + per_cta - 1) / per_cta, a.n_masks), dim3(kAllRowsWarps * 32), smem2, s,

@@ -117,6 +117,69 @@ __device__ __forceinline__ float dot_row_rot(const unsigned char* row, int swz, 
     return acc;
 }
 
+// Both branches' rotated dots of one staged bf16 row in one pass (the same operations
+// as dot_row_rot, element for element): 16-byte chunks c (x = elements 8c..8c+7) and
+// c + 8 (y = their rotation partners) are unpacked once, the cos/sin of the two key
+// positions come as float4 pairs (L1 broadcast), and the two accumulators advance in
+// the reference's element order — first half (x*c - y*s), then second half (x*s + y*c).
+// plain1: branch 1's key position is 0 (the relative policy, rope_policy.cpp:37-57) —
+// cos 1 and sin 0 exactly in the table, so x*1 - y*0 == x and x*0 + y*1 == y (up to the
+// sign of a zero, which no comparison sees) and branch 1 is the unrotated dot.
+__device__ __forceinline__ void dot_row_rot2_bf16(const unsigned char* row, int swz, const float* q,
+                                                  const float* cs1, const float* sn1, const float* cs2,
+                                                  const float* sn2, bool same, float& out1, float& out2,
+                                                  bool plain1 = false) {
+    float a1 = 0.0f, a2 = 0.0f;
+#pragma unroll
+    for (int part = 0; part < 2; ++part) {  // 0: r_i = x c - y s (i < 64); 1: r = x s + y c
+#pragma unroll 2
+        for (int c = 0; c < 8; ++c) {
+            const uint4 xv = *reinterpret_cast<const uint4*>(row + ((c ^ swz) << 4));
+            const uint4 yv = *reinterpret_cast<const uint4*>(row + (((c + 8) ^ swz) << 4));
+            const float x[8] = {bf16_lo(xv.x), bf16_hi(xv.x), bf16_lo(xv.y), bf16_hi(xv.y),
+                                bf16_lo(xv.z), bf16_hi(xv.z), bf16_lo(xv.w), bf16_hi(xv.w)};
+            const float y[8] = {bf16_lo(yv.x), bf16_hi(yv.x), bf16_lo(yv.y), bf16_hi(yv.y),
+                                bf16_lo(yv.z), bf16_hi(yv.z), bf16_lo(yv.w), bf16_hi(yv.w)};
+            const float4 qa = *reinterpret_cast<const float4*>(q + part * 64 + 8 * c);
+            const float4 qb = *reinterpret_cast<const float4*>(q + part * 64 + 8 * c + 4);
+            const float qq[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+            if (plain1) {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) a1 = __fadd_rn(a1, __fmul_rn(qq[e], part == 0 ? x[e] : y[e]));
+            } else {
+                const float4 c1a = __ldg(reinterpret_cast<const float4*>(cs1 + 8 * c));
+                const float4 c1b = __ldg(reinterpret_cast<const float4*>(cs1 + 8 * c + 4));
+                const float4 s1a = __ldg(reinterpret_cast<const float4*>(sn1 + 8 * c));
+                const float4 s1b = __ldg(reinterpret_cast<const float4*>(sn1 + 8 * c + 4));
+                const float cc1[8] = {c1a.x, c1a.y, c1a.z, c1a.w, c1b.x, c1b.y, c1b.z, c1b.w};
+                const float ss1[8] = {s1a.x, s1a.y, s1a.z, s1a.w, s1b.x, s1b.y, s1b.z, s1b.w};
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const float r = part == 0 ? __fsub_rn(__fmul_rn(x[e], cc1[e]), __fmul_rn(y[e], ss1[e]))
+                                              : __fadd_rn(__fmul_rn(x[e], ss1[e]), __fmul_rn(y[e], cc1[e]));
+                    a1 = __fadd_rn(a1, __fmul_rn(qq[e], r));
+                }
+            }
+            if (!same) {
+                const float4 c2a = __ldg(reinterpret_cast<const float4*>(cs2 + 8 * c));
+                const float4 c2b = __ldg(reinterpret_cast<const float4*>(cs2 + 8 * c + 4));
+                const float4 s2a = __ldg(reinterpret_cast<const float4*>(sn2 + 8 * c));
+                const float4 s2b = __ldg(reinterpret_cast<const float4*>(sn2 + 8 * c + 4));
+                const float cc2[8] = {c2a.x, c2a.y, c2a.z, c2a.w, c2b.x, c2b.y, c2b.z, c2b.w};
+                const float ss2[8] = {s2a.x, s2a.y, s2a.z, s2a.w, s2b.x, s2b.y, s2b.z, s2b.w};
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const float r = part == 0 ? __fsub_rn(__fmul_rn(x[e], cc2[e]), __fmul_rn(y[e], ss2[e]))
+                                              : __fadd_rn(__fmul_rn(x[e], ss2[e]), __fmul_rn(y[e], cc2[e]));
+                    a2 = __fadd_rn(a2, __fmul_rn(qq[e], r));
+                }
+            }
+        }
+    }
+    out1 = a1;
+    out2 = same ? a1 : a2;
+}
+
 // ------------------------------------------------------------------------ staging
 template <typename T>
 struct RowGeom {

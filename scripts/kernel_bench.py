@@ -13,7 +13,11 @@ stages = [(64, 256, 32768), (64, 32, 8192), (64, 8, 2048)]
 q, k, v = synth.generate(groups * hpm, groups, t, d, seed=1)
 kv = D.PagedKV(k, v, page_size=64)
 del k, v
-layer = D.FusedDecodeLayer(kv, stages, sink=256, stream_tokens=1024, n_q_heads=groups * hpm, n_masks=groups)
+import os
+ext = os.environ.get("EXT") == "1"
+rope = D.RopeTable(t + 2, d) if ext else None
+layer = D.FusedDecodeLayer(kv, stages, sink=256, stream_tokens=1024, n_q_heads=groups * hpm, n_masks=groups,
+                           policy=D.RopePolicy(extension=ext), rope=rope)
 layer.q.copy_(q.view(layer.q.shape))
 layer.run(t)
 torch.cuda.synchronize()

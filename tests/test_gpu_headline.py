@@ -32,13 +32,14 @@ SINK, STREAM = 256, 1024
 GROUPS, HPM, D = 8, 4, 128
 
 
-def _run(t, seed, fused=True):
+def _run(t, seed, fused=True, ext=False, layer1=4):
     from paper_2502_08910_b200 import device as Dv, synth
     Dv.require_cuda()
     q, k, v = synth.generate(GROUPS * HPM, GROUPS, t, D, seed=seed)
     kv = Dv.PagedKV(k, v, page_size=64, dtype=torch.bfloat16)
+    rope = Dv.RopeTable(t + 2, D) if ext else None
     layer = Dv.FusedDecodeLayer(kv, STAGES, sink=SINK, stream_tokens=STREAM, n_q_heads=GROUPS * HPM,
-                                n_masks=GROUPS)
+                                n_masks=GROUPS, layer1=layer1, policy=Dv.RopePolicy(extension=ext), rope=rope)
     # "always": every refresh pattern on hp_decode_layer (the default takes the per-stage
     # kernels for steps that refresh no stage with a successor); False: per-stage kernels only
     layer._fused = "always" if fused else False
@@ -48,7 +49,7 @@ def _run(t, seed, fused=True):
     return q, k, v, layer, out
 
 
-def _check_groups(port, t, q, k, v, layer, out):
+def _check_groups(port, t, q, k, v, layer, out, ext=False, layer1=4):
     qh = q[:, 0].cpu().numpy().reshape(GROUPS, HPM, D)
     o = out.cpu().numpy().reshape(GROUPS, HPM, D)
     for g in range(GROUPS):
@@ -58,11 +59,13 @@ def _check_groups(port, t, q, k, v, layer, out):
         # stage by stage (the stage caches), chained as DecodeEngine::step does
         cur = np.arange(SINK, t - STREAM, dtype=np.int64)
         for i, st in enumerate(STAGES):
-            cur = port.run_pruning_stage(st, cur, qg, kg, stream=STREAM, qstart=t - 1)
+            cur = port.run_pruning_stage(st, cur, qg, kg, stream=STREAM, qstart=t - 1, ext=ext, layer1=layer1,
+                                         rope_max=t + 2)
             cl, cc = layer.mask(i)
             got = cl[g, : int(cc[g])].cpu().numpy()
             assert np.array_equal(got, cur), (g, i, len(got), len(cur))
-        masks, want, _ = port.decode_layer_step(qh[g: g + 1], kg, vg, STAGES, sink=SINK, stream=STREAM)
+        masks, want, _ = port.decode_layer_step(qh[g: g + 1], kg, vg, STAGES, sink=SINK, stream=STREAM, ext=ext,
+                                                layer1=layer1)
         assert np.array_equal(masks[0], cur), g
         err = np.abs(o[g].astype(np.float64) - want[0]).max() / max(1e-6, np.abs(want[0]).max())
         assert err <= RTOL, (g, err)
@@ -102,3 +105,16 @@ def test_c2_128k_8groups_exact(port, path):
     q, k, v, layer, out = _run(t, seed=2, fused=path == "layer")
     assert all(x is not None for x in layer.dispatch())
     _check_groups(port, t, q, k, v, layer, out)
+
+
+@pytest.mark.parametrize("layer1", [2, 4])  # chunk-indexed (one rotation) / relative (two per row)
+def test_headline_1m_8groups_rope_extension_exact(port, layer1):
+    """RoPE extension on at the C3 shape: the one-wave stage-1 kernel and the all-rows
+    stage-3 kernel rotate every key row inside the sequential dot (rope_policy.cpp:18-72,
+    pruning.cpp:39-67) and the BSA uses streaming positions (sparse_attention.cpp:43-50):
+    every stage list and mask index-exact, outputs within 1e-3."""
+    t = 1 << 20
+    q, k, v, layer, out = _run(t, seed=3, fused=False, ext=True, layer1=layer1)
+    kinds = layer.dispatch()
+    assert kinds[0] == "wide" and kinds[2] == "allrows", kinds
+    _check_groups(port, t, q, k, v, layer, out, ext=True, layer1=layer1)
