@@ -58,6 +58,7 @@ def parse():
                    help="layers per decode step (distinct KV each); value = step time / layers")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-ext", action="store_true", help="skip the RoPE-extension step (ext_on_us)")
+    p.add_argument("--no-offload", action="store_true", help="skip the host-offloaded KV run (offload)")
     p.add_argument("--shard-of", type=int, default=0,
                    help="dev: run as rank 0 of an N-way KV-group split in ONE process (no process "
                         "group) to measure one GPU's share of the N-GPU step")
@@ -373,6 +374,49 @@ def main():
             ext_us = tt.item()
         del ext_layers, rope, eg
 
+    # ---- C3 with host-offloaded KV (BASELINE configs[2]): one layer of this rank's groups
+    # with K/V in pinned host memory behind the on-GPU LRU page cache (CachedKV, half of
+    # the pages resident, warm with the most recent ones), the (16, 8, 4) schedule for two
+    # whole cycles, a step-end commit per step; misses are read over the host link inside
+    # the gathers and installed by the commit
+    offload = None
+    if not args.no_offload:
+        parts = [synth.generate(HPM, 1, t, D, seed=1 + g, device=dev) for g in range(g0, g1)]
+        k_h = torch.cat([x[1] for x in parts])
+        v_h = torch.cat([x[2] for x in parts])
+        q_o = torch.cat([x[0] for x in parts])[:, 0]
+        del parts
+        frac = 0.5
+        ckv = D_.CachedKV(k_h, v_h, num_slots=int(frac * D_.ceil_div(t, 64)), page_size=64, device=dev)
+        del k_h, v_h
+        ol = D_.FusedDecodeLayer(ckv, STAGES, sink=SINK, stream_tokens=STREAM, n_q_heads=ng * HPM, n_masks=ng,
+                                 device=dev)
+        ol.q.copy_(q_o)
+        ctr = [0, 0, 0]
+        ot, kinds = [], []
+        for i in range(32):
+            fl = [c == 0 for c in ctr]
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(cur)
+            ol.run(t, refresh=fl)
+            ckv.commit()
+            b.record(cur)
+            b.synchronize()
+            ot.append(1000.0 * a.elapsed_time(b))
+            kinds.append(tuple(fl))
+            ctr = [(c + 1) % r for c, r in zip(ctr, REFRESH)]
+        st = ckv.stats.cpu().tolist()
+        full_o = [x for x, kd in zip(ot, kinds) if all(kd)]
+        bsa_o = sorted(x for x, kd in zip(ot, kinds) if not any(kd))
+        offload = {"cache_fraction": frac, "layers": 1, "steps": len(ot),
+                   "mean_step_us": statistics.mean(ot[16:]), "full_refresh_us": full_o,
+                   "bsa_only_us_median": bsa_o[len(bsa_o) // 2] if bsa_o else None,
+                   "hits": st[0], "misses": st[1], "evictions": st[2],
+                   "hit_ratio": st[0] / max(1, st[0] + st[1]),
+                   "note": "µs per layer step incl. the step-end LRU commit; second cycle averaged"}
+        del ol, ckv
+        torch.cuda.empty_cache()
+
     # ---- dominant kernel: the stage-1 descent (decode_stage_kernel), timed alone on its
     # stream: a graph of its L per-layer launches, L2 flushed before each replay
     s1_graph = torch.cuda.CUDAGraph()
@@ -490,6 +534,7 @@ def main():
             "amortized_us": amort_us,
             "amortized_schedule": "refresh (16, 8, 4), averaged over whole cycles",
             "bsa_only_us": bsa_us, "allgather_us": allgather_us,
+            "offload": offload,
             "ext_on_us": ext_us, "ext_on_note": "full-refresh step with RoPE extension on (layer 4: relative "
                                                 "pruning positions, two rotated dots per key row; streaming BSA)",
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -222,59 +222,6 @@ decode_stage_kernel(const hp_decode_stage_args a, float* scores, int* tickets, i
 // not), then makes two comparisons: l_c = 32 takes 3 rounds (2 + 3 + 3 rows) instead
 // of 6. The three dots run as independent chains over one q read. Same comparisons
 // on the same fp32 values as the classic kernel, so the same representatives.
-constexpr int kLookSlots = 3;
-
-__device__ __forceinline__ void dot3_bf16x(const unsigned char* r0, const unsigned char* r1, const unsigned char* r2,
-                                           int swz, const uint32_t* qb, float& d0, float& d1, float& d2) {
-    const uint4* q4 = reinterpret_cast<const uint4*>(qb);
-    float a0 = 0.f, a1 = 0.f, a2 = 0.f;
-#pragma unroll 2
-    for (int c = 0; c < 16; ++c) {
-        const int o = (c ^ swz) << 4;
-        const uint4 q = q4[c];
-        const uint4 x = *reinterpret_cast<const uint4*>(r0 + o);
-        const uint4 y = *reinterpret_cast<const uint4*>(r1 + o);
-        const uint4 z = *reinterpret_cast<const uint4*>(r2 + o);
-        a0 = fma_bf16(q.x, x.x, a0, false); a1 = fma_bf16(q.x, y.x, a1, false); a2 = fma_bf16(q.x, z.x, a2, false);
-        a0 = fma_bf16(q.x, x.x, a0, true);  a1 = fma_bf16(q.x, y.x, a1, true);  a2 = fma_bf16(q.x, z.x, a2, true);
-        a0 = fma_bf16(q.y, x.y, a0, false); a1 = fma_bf16(q.y, y.y, a1, false); a2 = fma_bf16(q.y, z.y, a2, false);
-        a0 = fma_bf16(q.y, x.y, a0, true);  a1 = fma_bf16(q.y, y.y, a1, true);  a2 = fma_bf16(q.y, z.y, a2, true);
-        a0 = fma_bf16(q.z, x.z, a0, false); a1 = fma_bf16(q.z, y.z, a1, false); a2 = fma_bf16(q.z, z.z, a2, false);
-        a0 = fma_bf16(q.z, x.z, a0, true);  a1 = fma_bf16(q.z, y.z, a1, true);  a2 = fma_bf16(q.z, z.z, a2, true);
-        a0 = fma_bf16(q.w, x.w, a0, false); a1 = fma_bf16(q.w, y.w, a1, false); a2 = fma_bf16(q.w, z.w, a2, false);
-        a0 = fma_bf16(q.w, x.w, a0, true);  a1 = fma_bf16(q.w, y.w, a1, true);  a2 = fma_bf16(q.w, z.w, a2, true);
-    }
-    d0 = a0; d1 = a1; d2 = a2;
-}
-
-// up to three rows per lane (tok < 0 = none) into slots s * 32 + lane; whole warp calls
-template <bool WAIT = true>
-__device__ __forceinline__ void stage_rows3(const hp_kv_view& kv, int kvh, int64_t t0, int64_t t1, int64_t t2,
-                                            unsigned char* wstage, int lane) {
-    using G = RowGeom<bf16_t>;
-    constexpr int chunks = G::bytes / 16;
-    constexpr int rows_per_instr = 32 / chunks;
-    const int c = lane % chunks, sub = lane / chunks;
-    const int64_t tk[kLookSlots] = {t0, t1, t2};
-#pragma unroll
-    for (int sl = 0; sl < kLookSlots; ++sl) {
-        const char* p = tk[sl] >= 0 ? kv_row_ptr(kv, kv.k_pool, kv.k_host, kvh, tk[sl], 2) : nullptr;
-        const unsigned long long pu = reinterpret_cast<unsigned long long>(p);
-        unsigned char* base = wstage + static_cast<size_t>(sl) * 32 * G::stride;
-#pragma unroll
-        for (int r = 0; r < 32; r += rows_per_instr) {
-            const int row = r + sub;
-            const unsigned long long pp = __shfl_sync(0xffffffffu, pu, row);
-            if (pp) cp_async16(base + row * G::stride + ((c ^ (row & (chunks - 1))) << 4),
-                               reinterpret_cast<const char*>(pp) + (c << 4));
-        }
-    }
-    if constexpr (WAIT) {
-        cp_async_wait_all();
-        __syncwarp();
-    }
-}
-
 __global__ void __launch_bounds__(kStageWarps * 32, 2)
 decode_stage_look_kernel(const hp_decode_stage_args a, float* scores, int cg, int prefetch) {
     pdl_trigger();
