@@ -2,8 +2,7 @@
  * hipprune_b200 developer hooks — NOT part of the product ABI. Exported only by the
  * dev builds of the kernel library (HP_TRACE=1 / HP_VARIANT builds of
  * paper_2502_08910_b200/build.py, which define HP_TRACE or HP_DEV); the product
- * libhipprune_b200.so has none of these symbols. Used by scripts/ (timelines, phase cuts,
- * A/B of the layer kernel's cluster mode).
+ * libhipprune_b200.so has none of these symbols. Used by scripts/ (timelines, phase cuts).
  */
 #ifndef HIPPRUNE_B200_DEV_H
 #define HIPPRUNE_B200_DEV_H
@@ -21,8 +20,6 @@ int hp_layer_trace_enable(unsigned long long* buf, int kernel_id);
 int hp_debug_cut(int kernel_id, int at);
 /* the tcgen05 prefill's thread 0 writes progress codes to this mapped host word */
 int hp_debug_prefill_progress(int* mapped_word);
-/* hp_decode_layer: > 0 = thread-block-cluster mode of that size, <= 0 = persistent grid */
-int hp_decode_layer_cluster(int cs);
 
 #ifdef __cplusplus
 }

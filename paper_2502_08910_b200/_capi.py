@@ -192,9 +192,6 @@ def lib():
     L.hp_decode_layer_supported.argtypes = [C.POINTER(DecodeLayerArgs)]
     L.hp_decode_layer.restype = C.c_int
     L.hp_decode_layer.argtypes = [C.POINTER(DecodeLayerArgs), C.c_void_p]
-    if hasattr(L, "hp_decode_layer_cluster"):  # dev builds only (include/hipprune_b200_dev.h)
-        L.hp_decode_layer_cluster.restype = C.c_int
-        L.hp_decode_layer_cluster.argtypes = [C.c_int]
     L.hp_decode_materialize.restype = C.c_int
     L.hp_decode_materialize.argtypes = [C.POINTER(ListRef), C.POINTER(C.c_void_p),
                                         C.POINTER(C.c_void_p), C.POINTER(C.c_int64), C.c_int32,

@@ -6,24 +6,26 @@
 //   identity, descent, top-K       pruning.cpp:69-98,153-200 (Alg. 3, stable top-K)
 //   selected set, attention_row    sparse_attention.cpp:15-60,95-112
 //
-// B200 mapping. After stage 0 (131K independent descents at 1M: the one-wave kernel
-// of decode.cu, HBM-bound), the rest of a layer step is a chain of small dependent
-// pieces: stage-0 top-K, stage-1 descents (4K per KV group), top-K, stage-2 all-rows
-// scoring, top-K, and a 3.3K-key attention with a split-K merge. As separate kernels
-// every link pays a launch + drain; here a thread-block cluster owns one KV group
-// and every link is a cluster barrier (~0.2 us):
-//   * each CTA scores its slice of the stage's chunks (16 warps, lane = chunk,
-//     32 rows staged per warp with 16-byte cp.async, exact sequential fp32 dots)
-//     and pushes the chunk keys (max over the group's heads, order-mapped) into
-//     EVERY CTA's shared memory (st.shared::cluster);
-//   * one cluster barrier, then every CTA runs the same exact radix top-K on the
-//     full key set (cta_topk_smem), so all CTAs hold the kept chunk ids and can
-//     resolve the next stage's input positions through shared memory;
-//   * the attention splits the selected positions over the CTAs, each CTA gathers
-//     its K/V rows (cp.async), keeps an online softmax per head, and the partial
-//     (m, l, o) triples merge over distributed shared memory.
-// Key buffers alternate between two halves by stage so a fast CTA's pushes for
-// stage i+1 can never land in a buffer a slow CTA is still selecting from.
+// B200 mapping. After stage 0 (131K independent descents at 1M: the one-wave kernel of
+// decode.cu, HBM-bound), the rest of a layer step is a chain of small dependent pieces:
+// stage-0 top-K, stage-1 descents (4K per KV group), top-K, stage-2 all-rows scoring,
+// top-K, and a 3.3K-key attention with a split-K merge. As separate kernels every link
+// pays a launch and a drain. Here a persistent grid owns the layer: n_SM / n_groups
+// co-resident CTAs per KV group (one per SM: 18 per group for 8 groups, all 148 for one
+// group — the 8-GPU KV-group split), and every link is a group barrier in L2:
+//   * each CTA scores its slice of the stage's chunks — Alg. 3 descents (lane = chunk,
+//     32 rows staged per warp with 16-byte cp.async), or all-rows scoring for l_c <= 8 —
+//     and writes the chunk keys (max over the group's heads, order-mapped) to L2;
+//   * one group barrier, every CTA copies the full key set and runs the same exact
+//     radix top-K, so all hold the kept chunk ids and resolve the next stage's input
+//     through shared memory;
+//   * the attention splits the selected positions over the CTAs (K/V gathered by
+//     cp.async, QK^T and PV on mma.sync with bf16 hi/lo splits of q and p), the sink and
+//     stream rows having been prefetched into L2 while the stages ran; partials (m, l, o)
+//     go to L2 and the last CTA (acq_rel ticket) merges them.
+// Measured and dropped: one thread-block cluster per group with DSMEM exchanges (8 CTAs
+// per group: 107.8 vs 98.8 us per full-refresh layer — the phases are issue/latency
+// bound on 8 SMs; 16-CTA clusters do not all fit).
 
 #include <algorithm>
 #include <cstdlib>
@@ -37,45 +39,50 @@ using namespace hpk::dec;
 
 namespace {
 
-constexpr int kLT = 512;                           // threads per CTA
-constexpr int kLW = kLT / 32;                      // warps per CTA
-constexpr int kRow = kD * 2;                       // bf16 row bytes
-constexpr int kStageBytes = kLW * 32 * kRow;       // 128 KB: 32 rows per warp, or a K/V tile
-constexpr int kTile = kStageBytes / (2 * kRow);    // 256 keys (K + V) per attention tile
+constexpr int kLT = 512;                              // threads per CTA
+constexpr int kLW = kLT / 32;                         // warps per CTA
+constexpr int kRow = kD * 2;                          // bf16 row bytes
+constexpr int kSlot = 32 * kRow;                      // one 32-row staging slot (8 KB)
+constexpr int kTile = 256;                            // attention keys per tile (K + V = 128 KB)
+constexpr int kTileKV = 2 * kTile * kRow;             // 128 KB
+// 140 KB: 16 warps x 8 KB of descent staging, or the attention tile + row pointers + p
+constexpr int kStageBytes = kTileKV + 2 * kTile * 8 + 8 * kTile * 4;
 constexpr int kMaxS = 4;
-constexpr int kPart = kD + 2;                      // partial record: o[128], m, l
+constexpr int kPart = kD + 2;                         // partial record: o[128], m, l
+constexpr int kKeysMax = 16384;                       // chunk keys per stage selection
+constexpr int kMaxGroupCtas = 160;                    // CTAs per KV group
+constexpr int kBarInts = 4;                           // per mask: arrivals, generation, merge ticket, pad
 
 __host__ __device__ __forceinline__ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct LayerParams {
     hp_decode_layer_args a;
-    uint32_t* gkeys;          // grid mode: [2][n_masks][keys_cap] exchanged chunk keys
-    float* gpart;             // grid mode: [n_masks][CTAs][HP][kPart] attention partials
-    int* gbar;                // grid mode: [n_masks][4] barrier count, generation, merge ticket (see group_barrier)
+    uint32_t* gkeys;          // [2][n_masks][keys_cap] exchanged chunk keys (stage parity)
+    float* gpart;             // [n_masks][CTAs][HP][kPart] attention partials
+    int* gbar;                // [n_masks][kBarInts]
     const float* scores0;     // stage-0 chunk scores [m][planes0][max_chunks0]
     int32_t planes0;
     int32_t max_chunks0;
     int64_t n0;               // stage-0 input length
-    int32_t keys_cap;         // order keys per buffer (two buffers)
+    int32_t keys_cap;         // order keys per buffer
     int32_t red_cap;          // per-head descent scores per CTA
     int32_t sel_off[kMaxS];   // offsets (ints) of each stage's kept ids in the shared sel area
     int32_t sel_total;
 };
 
+// Shared memory: the staging region is reused by phase — descents (a 32-row slot per
+// warp), the selection's key copy (offset 0), the attention tile (K/V at 0, row pointers
+// and probabilities behind it), the merge's staged partials; then the small arrays.
 struct LayerSmem {
-    size_t keys, sel, qs, qb, red, tok, pw, part, bytes;
-    // cluster mode double-buffers the keys in shared memory (peers push the next stage's
-    // keys while a slow CTA still selects); grid mode exchanges through L2 (double-buffered
-    // there) and needs one shared copy
-    __host__ __device__ LayerSmem(int keys_cap, int sel_total, int hp, int red_cap, int key_bufs) {
+    size_t ptrs, pw, sel, qs, qb, red, part, bytes;
+    __host__ __device__ LayerSmem(int sel_total, int hp, int red_cap) {
+        ptrs = kTileKV;                                      // K and V row pointers [2][kTile]
+        pw = ptrs + 2 * kTile * 8;                           // [hp][kTile] scores / probabilities
         size_t o = kStageBytes;
-        keys = o; o += align_up(static_cast<size_t>(key_bufs) * keys_cap * 4, 16);
         sel = o; o += align_up(static_cast<size_t>(sel_total) * 4, 16);
         qs = o; o += static_cast<size_t>(hp) * kD * 4;
         qb = o; o += static_cast<size_t>(hp) * kD * 2;
         red = o; o += align_up(static_cast<size_t>(hp) * red_cap * 4, 16);
-        tok = o; o += kTile * 16;  // K and V row pointers of the tile's keys
-        pw = o; o += static_cast<size_t>(hp) * kTile * 4;
         part = o; o += align_up(static_cast<size_t>(hp) * kPart * 4, 16);
         bytes = o;
     }
@@ -87,13 +94,13 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
     return r;
 }
 
-// D += A B, m16n8k16, bf16 inputs, fp32 accumulate (a1/a3: rows 8..15, unused here)
-__device__ __forceinline__ void mma_bf16_16816(float& d0, float& d1, float& d2, float& d3, uint32_t a0, uint32_t a1,
-                                               uint32_t a2, uint32_t a3, uint32_t b0, uint32_t b1) {
+// D += A B, m16n8k16, bf16 inputs, fp32 accumulate (rows 8..15 of A unused here)
+__device__ __forceinline__ void mma_bf16_16816(float& d0, float& d1, float& d2, float& d3, uint32_t a0, uint32_t a2,
+                                               uint32_t b0, uint32_t b1) {
     asm volatile(
         "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
         : "+f"(d0), "+f"(d1), "+f"(d2), "+f"(d3)
-        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+        : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
 }
 
 __device__ __forceinline__ void ldmatrix_x4_trans(uint32_t* r, const void* p) {
@@ -102,12 +109,11 @@ __device__ __forceinline__ void ldmatrix_x4_trans(uint32_t* r, const void* p) {
                  : "r"(smem_u32(p)));
 }
 
-// Group barrier over the n CTAs of one KV group (grid mode), sense-reversing: bar[0]
-// counts arrivals, bar[1] is the generation. Each CTA read the generation once at
-// kernel start (gen, tracked locally after that); it arrives (acq_rel), the last
-// arrival zeroes the count and publishes gen + 1 (release), the others spin (acquire)
-// until it appears. The count is back at 0 after every barrier, so consecutive
-// launches need no reset. Also a ticket (bar[2]) for the last-CTA merge.
+// Group barrier over the n CTAs of one KV group, sense-reversing: bar[0] counts
+// arrivals, bar[1] is the generation. Each CTA read the generation once at kernel start
+// (tracked locally after that); it arrives (acq_rel), the last arrival zeroes the count
+// and publishes gen + 1 (release), the others spin (acquire) until it appears. The
+// count is back at 0 after every barrier, so consecutive launches need no reset.
 __device__ __forceinline__ void group_barrier(int* bar, int n, int& gen) {
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -127,42 +133,35 @@ __device__ __forceinline__ void group_barrier(int* bar, int n, int& gen) {
     __syncthreads();
 }
 
-// CLU: a thread-block cluster per KV group (exchanges over DSMEM, cluster barriers).
-// !CLU (grid mode): a persistent grid of ~n_SM / n_masks CTAs per group, one CTA per SM,
-// all co-resident; exchanges through L2 and group barriers. Same arithmetic either way.
-template <int HP, bool CLU>
+template <int HP>
 __global__ void __launch_bounds__(kLT, 1) decode_layer_kernel(const LayerParams P) {
-    if constexpr (CLU) pdl_trigger();  // grid mode triggers after its last barrier
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ TopkShared tsh;
     __shared__ float sh_m[HP], sh_l[HP], sh_alpha[HP];
+    __shared__ int sh_last;
     const hp_decode_layer_args& a = P.a;
     const int m = blockIdx.y;
-    const unsigned rank = CLU ? cluster_ctarank() : blockIdx.x;
-    const unsigned CS = CLU ? cluster_nctarank() : gridDim.x;
-    int* gbar = P.gbar + 4 * m;
-    int gen = 0;
+    const unsigned rank = blockIdx.x, CS = gridDim.x;
     const int t = threadIdx.x, lane = t & 31, w = warp_id();
-    const LayerSmem L(P.keys_cap, P.sel_total, HP, P.red_cap, CLU ? 2 : 1);
+    const LayerSmem L(P.sel_total, HP, P.red_cap);
     unsigned char* stage = smem;
-    uint32_t* keys_buf = reinterpret_cast<uint32_t*>(smem + L.keys);
+    uint32_t* keys = reinterpret_cast<uint32_t*>(smem);  // the selection's copy (staging is idle then)
+    const char** kptr = reinterpret_cast<const char**>(smem + L.ptrs);
+    const char** vptr = kptr + kTile;
+    float* pw = reinterpret_cast<float*>(smem + L.pw);
     int32_t* sel = reinterpret_cast<int32_t*>(smem + L.sel);
     float* qs = reinterpret_cast<float*>(smem + L.qs);
     uint32_t* qb = reinterpret_cast<uint32_t*>(smem + L.qb);
     float* red = reinterpret_cast<float*>(smem + L.red);
-    const char** kptr = reinterpret_cast<const char**>(smem + L.tok);
-    const char** vptr = kptr + kTile;
-    float* pw = reinterpret_cast<float*>(smem + L.pw);
     float* part = reinterpret_cast<float*>(smem + L.part);
-    const int kv_group = a.n_q_heads / a.kv.n_kv;
-    const int kvh = (m * HP) / kv_group;  // the mask's heads share one kv head (host-checked)
+    const int kvh = (m * HP) / (a.n_q_heads / a.kv.n_kv);  // the mask's heads share one kv head (host-checked)
+    int* gbar = P.gbar + kBarInts * m;
+    int gen = 0;
 
     trace(20, 0);
     pdl_wait();
-    if constexpr (!CLU) {  // this launch's starting generation (no barrier can complete before we arrive)
-        if (t == 0) asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(gen) : "l"(gbar + 1) : "memory");
-        gen = __shfl_sync(0xffffffffu, gen, 0);
-    }
+    if (t == 0) asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(gen) : "l"(gbar + 1) : "memory");
+    gen = __shfl_sync(0xffffffffu, gen, 0);  // this launch's starting generation (no barrier completes before we arrive)
     bool safe = true;
     for (int i = t; i < HP * kD; i += kLT) {
         const float x = a.q[static_cast<int64_t>(m * HP) * kD + i];
@@ -173,6 +172,21 @@ __global__ void __launch_bounds__(kLT, 1) decode_layer_kernel(const LayerParams 
     const bool use_fma = __syncthreads_and(safe) && a.keys_exact != nullptr && *a.keys_exact != 0;
     for (int i = t; i < HP * kD / 2; i += kLT)
         qb[i] = (__float_as_uint(qs[2 * i]) >> 16) | (__float_as_uint(qs[2 * i + 1]) & 0xffff0000u);
+
+    // the attention's sink and stream rows are known now: warm them into L2 while the
+    // stages run (the group's CTAs split them; K and V, two 128 B lines per row)
+    const int64_t pos = a.query_position;
+    const int64_t sink_end = min64(a.sink_tokens, pos + 1);
+    const int64_t stream_begin = max64(pos + 1 > a.stream_tokens ? pos + 1 - a.stream_tokens : 0, sink_end);
+    {
+        const int64_t n_fixed = sink_end + (pos + 1 - stream_begin);
+        for (int64_t x = static_cast<int64_t>(rank) * kLT + t; x < n_fixed; x += static_cast<int64_t>(CS) * kLT) {
+            const int64_t tk = x < sink_end ? x : stream_begin + (x - sink_end);
+            const char* kp = kv_row_ptr(a.kv, a.kv.k_pool, a.kv.k_host, kvh, tk, 2);
+            const char* vp = kv_row_ptr(a.kv, a.kv.v_pool, a.kv.v_host, kvh, tk, 2);
+            prefetch_l2(kp); prefetch_l2(kp + 128); prefetch_l2(vp); prefetch_l2(vp + 128);
+        }
+    }
     __syncthreads();
     trace(20, 1);
 
@@ -188,19 +202,13 @@ __global__ void __launch_bounds__(kLT, 1) decode_layer_kernel(const LayerParams 
         }
         return a.sink_tokens + p;
     };
-    int buf = 0;  // key buffer parity: stage selections alternate between two buffers
-    auto push_key = [&](uint32_t* keys, int64_t c, uint32_t k) {
-        if constexpr (CLU) {
-            for (unsigned d = 0; d < CS; ++d) st_dsmem_u32(dsmem_addr(keys + c, d), k);
-        } else {
-            P.gkeys[(static_cast<size_t>(buf ^ 1) * a.n_masks + m) * P.keys_cap + c] = k;
-        }
+    int buf = 0;  // key buffer parity in L2: stage selections alternate between two buffers
+    auto put_key = [&](int64_t c, uint32_t k) {
+        P.gkeys[(static_cast<size_t>(buf) * a.n_masks + m) * P.keys_cap + c] = k;
     };
 
     const int S = a.n_stages;
     int64_t n_in = P.n0;
-    unsigned char* wstage = stage + static_cast<size_t>(w) * 32 * kRow;
-    const unsigned char* myrow = wstage + lane * kRow;
     const int swz = lane & 15;
     for (int i = 0; i < S; ++i) {
         if (!a.refresh[i]) {  // not due: the cached list stands (decode.cpp:241-249)
@@ -218,9 +226,6 @@ __global__ void __launch_bounds__(kLT, 1) decode_layer_kernel(const LayerParams 
             n_sel = static_cast<int>(cc);
             __syncthreads();
         } else {
-            const int gbuf = buf;  // global (grid mode) / shared (cluster mode) buffer of this stage
-            uint32_t* keys = CLU ? keys_buf + buf * P.keys_cap : keys_buf;
-            buf ^= 1;
             if (i == 1) trace(22, 0);
             if (i == 0) {
                 // stage 0's scores (decode.cu descent kernels): this CTA's slice, max over heads
@@ -235,7 +240,7 @@ __global__ void __launch_bounds__(kLT, 1) decode_layer_kernel(const LayerParams 
                     float best = -INFINITY;
 #pragma unroll
                     for (int h = 0; h < 8; ++h) best = (best < v[h]) ? v[h] : best;  // std::max in head order (pruning.cpp:182)
-                    push_key(keys, c, order_key(best));
+                    put_key(c, order_key(best));
                 }
             } else if (lc <= 8 && 32 % lc == 0) {
                 // short chunks: a warp item = 32 / lc whole chunks, lane = row; one gather for
@@ -248,6 +253,8 @@ __global__ void __launch_bounds__(kLT, 1) decode_layer_kernel(const LayerParams 
                 int iters = 0;
                 while ((1 << iters) < lc) ++iters;
                 const int cl = lane / lc, r = lane - cl * lc, c0l = cl * lc;
+                unsigned char* wstage = stage + static_cast<size_t>(w) * kSlot;
+                const unsigned char* myrow = wstage + lane * kRow;
                 for (int k = 0; k < per_warp; ++k) {
                     const int64_t item = i0 + w + static_cast<int64_t>(k) * kLW;
                     const int64_t j = item * cpw + cl;
@@ -296,17 +303,21 @@ __global__ void __launch_bounds__(kLT, 1) decode_layer_kernel(const LayerParams 
                         }
                         best = (best < s1) ? s1 : best;  // max over heads in head order
                     }
-                    if (live && r == 0) push_key(keys, j, order_key(best));
+                    if (live && r == 0) put_key(j, order_key(best));
                 }
             } else {
-                // descents: a warp item = (32-chunk group, head), lane = chunk (Alg. 3,
-                // one dependent row gather per comparison)
+                // descents: a warp item = (32-chunk group, head), lane = chunk (Alg. 3, one
+                // dependent row gather per comparison). (The two-comparison lookahead rounds of
+                // decode_stage_look_kernel were measured slower here: 22.5 vs 17 us for stage 2
+                // at 1M — 3x the rows per round on 8 warps per SM.)
                 const int64_t n_groups = (cc + 31) / 32;
                 const int64_t gpc = (n_groups + CS - 1) / CS;
                 const int64_t g0 = static_cast<int64_t>(rank) * gpc;
                 const int my_groups = static_cast<int>(max64(0, min64(n_groups, g0 + gpc) - g0));
                 const int n_items = my_groups * HP;
                 const int per_warp = (n_items + kLW - 1) / kLW;
+                unsigned char* wstage = stage + static_cast<size_t>(w) * kSlot;
+                const unsigned char* myrow = wstage + lane * kRow;
                 for (int k = 0; k < per_warp; ++k) {
                     const int item_raw = w + k * kLW;
                     const bool item_ok = item_raw < n_items;
@@ -355,40 +366,37 @@ __global__ void __launch_bounds__(kLT, 1) decode_layer_kernel(const LayerParams 
                         float best = -INFINITY;
 #pragma unroll
                         for (int h = 0; h < HP; ++h) {
-                            const float s = red[h * P.red_cap + c];
-                            best = (best < s) ? s : best;
+                            const float sv = red[h * P.red_cap + c];
+                            best = (best < sv) ? sv : best;
                         }
-                        push_key(keys, gc, order_key(best));
+                        put_key(gc, order_key(best));
                     }
                 }
             }
             if (i == 1) trace(22, 1);
-            if constexpr (CLU) {
-                cluster_sync_all();  // every CTA's keys landed everywhere
-            } else {
-                group_barrier(gbar, static_cast<int>(CS), gen);
-                if (i == 1) trace(22, 2);
-                const uint32_t* gk = P.gkeys + (static_cast<size_t>(gbuf) * a.n_masks + m) * P.keys_cap;
-                for (int64_t j0 = 0; j0 < cc; j0 += 8 * kLT) {  // 8 independent loads in flight per thread
-                    uint32_t v[8];
+            group_barrier(gbar, static_cast<int>(CS), gen);  // every CTA's keys are in L2
+            if (i == 1) trace(22, 2);
+            const uint32_t* gk = P.gkeys + (static_cast<size_t>(buf) * a.n_masks + m) * P.keys_cap;
+            for (int64_t j0 = 0; j0 < cc; j0 += 8 * kLT) {  // 8 independent loads in flight per thread
+                uint32_t v[8];
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const int64_t j = j0 + u * kLT + t;
-                        v[u] = j < cc ? __ldcg(gk + j) : 0u;
-                    }
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const int64_t j = j0 + u * kLT + t;
-                        if (j < cc) keys[j] = v[u];
-                    }
+                for (int u = 0; u < 8; ++u) {
+                    const int64_t j = j0 + u * kLT + t;
+                    v[u] = j < cc ? __ldcg(gk + j) : 0u;
                 }
-                __syncthreads();
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int64_t j = j0 + u * kLT + t;
+                    if (j < cc) keys[j] = v[u];
+                }
             }
+            __syncthreads();
             if (i == 1) trace(22, 3);
             cta_topk_smem(keys, static_cast<int>(cc), K, seli, tsh);
             if (i == 1) trace(22, 4);
             n_out = static_cast<int64_t>(K - 1) * lc + min64(lc, n_in - static_cast<int64_t>(seli[K - 1]) * lc);
             n_sel = K;
+            buf ^= 1;  // a fast CTA's next keys never land in a buffer a slow CTA still copies
         }
         if (rank == 0) {  // the stage's kept chunk ids and output length (the caches' source)
             for (int j = t; j < n_sel; j += kLT) a.sel[i][static_cast<int64_t>(m) * a.sel_stride[i] + j] = seli[j];
@@ -400,10 +408,7 @@ __global__ void __launch_bounds__(kLT, 1) decode_layer_kernel(const LayerParams 
 
     // ---- block-sparse attention over sinks ∪ last list ∪ stream (selected_indices +
     // attention_row, sparse_attention.cpp:15-60,95-112), the selected positions split
-    // over the cluster's CTAs
-    const int64_t pos = a.query_position;
-    const int64_t sink_end = min64(a.sink_tokens, pos + 1);
-    const int64_t stream_begin = max64(pos + 1 > a.stream_tokens ? pos + 1 - a.stream_tokens : 0, sink_end);
+    // over the group's CTAs
     const int64_t mc = n_in;
     const int64_t nsel = sink_end + mc + (pos + 1 - stream_begin);
     const int64_t per = (nsel + CS - 1) / CS;
@@ -416,18 +421,6 @@ __global__ void __launch_bounds__(kLT, 1) decode_layer_kernel(const LayerParams 
     // heads (HP <= 8 of 16), q and p split into bf16 hi + lo parts so the products carry
     // ~16 mantissa bits (fp32-grade vs the 1e-3 tolerance; K and V are bf16 exactly).
     const int g = lane >> 2, tq = lane & 3;
-    uint32_t qa_hi[8][2], qa_lo[8][2];  // A fragments of q for the 8 k-steps (rows g < HP)
-#pragma unroll
-    for (int ks = 0; ks < 8; ++ks) {
-#pragma unroll
-        for (int half = 0; half < 2; ++half) {
-            const int d = ks * 16 + half * 8 + 2 * tq;
-            const float x0 = g < HP ? qs[g * kD + d] : 0.f, x1 = g < HP ? qs[g * kD + d + 1] : 0.f;
-            const uint32_t h2 = pack_bf16(x0, x1);
-            qa_hi[ks][half] = h2;
-            qa_lo[ks][half] = pack_bf16(x0 - bf16_lo(h2), x1 - bf16_hi(h2));
-        }
-    }
     // P.V split: warp -> 16 output dims (two n-tiles) x one half of the tile's keys
     const int pv_n0 = (w & 7) * 16, pv_half = w >> 3;
     float oacc[2][2] = {{0.f, 0.f}, {0.f, 0.f}};  // rows g (< HP): dims pv_n0 + {0, 8} + 2tq + {0,1}
@@ -469,11 +462,20 @@ __global__ void __launch_bounds__(kLT, 1) decode_layer_kernel(const LayerParams 
             const unsigned char* kr = Ks + j * kRow;
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks) {
+                uint32_t ah[2], al[2];
+#pragma unroll
+                for (int half = 0; half < 2; ++half) {
+                    const int d = ks * 16 + half * 8 + 2 * tq;
+                    const float x0 = g < HP ? qs[g * kD + d] : 0.f, x1 = g < HP ? qs[g * kD + d + 1] : 0.f;
+                    const uint32_t h2 = pack_bf16(x0, x1);
+                    ah[half] = h2;
+                    al[half] = pack_bf16(x0 - bf16_lo(h2), x1 - bf16_hi(h2));
+                }
                 const int d0 = ks * 16 + 2 * tq, d1 = d0 + 8;
                 const uint32_t b0 = *reinterpret_cast<const uint32_t*>(kr + (((d0 >> 3) ^ (j & 15)) << 4) + (d0 & 7) * 2);
                 const uint32_t b1 = *reinterpret_cast<const uint32_t*>(kr + (((d1 >> 3) ^ (j & 15)) << 4) + (d1 & 7) * 2);
-                mma_bf16_16816(c0, c1, c2, c3, qa_hi[ks][0], 0u, qa_hi[ks][1], 0u, b0, b1);
-                mma_bf16_16816(c0, c1, c2, c3, qa_lo[ks][0], 0u, qa_lo[ks][1], 0u, b0, b1);
+                mma_bf16_16816(c0, c1, c2, c3, ah[0], ah[1], b0, b1);
+                mma_bf16_16816(c0, c1, c2, c3, al[0], al[1], b0, b1);
             }
             if (g < HP) {
                 const int jj = kt * 8 + 2 * tq;
@@ -527,16 +529,15 @@ __global__ void __launch_bounds__(kLT, 1) decode_layer_kernel(const LayerParams 
                     alo[half] = pack_bf16(p0_ - bf16_lo(h2), p1_ - bf16_hi(h2));
                 }
                 // ldmatrix.x4.trans: matrices (keys k0..+7 | k0+8..+15) x (dims n0 | n0+8)
-                const int r = lane & 15, nsel = lane >> 4;
-                const int jrow = k0 + r, cch = (pv_n0 >> 3) + nsel;
+                const int r = lane & 15, nsl = lane >> 4;
+                const int jrow = k0 + r, cch = (pv_n0 >> 3) + nsl;
                 uint32_t b[4];
                 ldmatrix_x4_trans(b, Vs + jrow * kRow + ((cch ^ (jrow & 15)) << 4));
-                // b[0], b[1]: n-tile 0 (k halves), b[2], b[3]: n-tile 1
 #pragma unroll
                 for (int nt = 0; nt < 2; ++nt) {
                     float d0 = oacc[nt][0], d1 = oacc[nt][1], d2 = 0.f, d3 = 0.f;
-                    mma_bf16_16816(d0, d1, d2, d3, ah[0], 0u, ah[1], 0u, b[2 * nt], b[2 * nt + 1]);
-                    mma_bf16_16816(d0, d1, d2, d3, alo[0], 0u, alo[1], 0u, b[2 * nt], b[2 * nt + 1]);
+                    mma_bf16_16816(d0, d1, d2, d3, ah[0], ah[1], b[2 * nt], b[2 * nt + 1]);
+                    mma_bf16_16816(d0, d1, d2, d3, alo[0], alo[1], b[2 * nt], b[2 * nt + 1]);
                     oacc[nt][0] = d0;
                     oacc[nt][1] = d1;
                 }
@@ -562,138 +563,98 @@ __global__ void __launch_bounds__(kLT, 1) decode_layer_kernel(const LayerParams 
         part[h * kPart + e] = pt2[h * kD + e] + pt2[(HP + h) * kD + e];
     }
     if (t < HP) { part[t * kPart + kD] = sh_m[t]; part[t * kPart + kD + 1] = sh_l[t]; }
+    __syncthreads();
     float* gp = P.gpart + static_cast<size_t>(m) * CS * HP * kPart;
-    if constexpr (CLU) {
-        cluster_sync_all();
-        // CTA r merges heads r, r + CS, ... over the cluster's partials (log-sum-exp, DSMEM)
-        for (int h = rank; h < HP; h += CS) {
+    for (int x = t; x < HP * kPart; x += kLT) gp[static_cast<size_t>(rank) * HP * kPart + x] = part[x];
+    float* allp = reinterpret_cast<float*>(stage);  // staged partials
+    if (static_cast<int>(CS) * HP * kPart * 4 <= kStageBytes) {
+        // the last CTA to finish (acq_rel ticket) merges every head: no CTA waits
+        __syncthreads();
+        if (t == 0) {
+            int prev;
+            asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(prev) : "l"(gbar + 2) : "memory");
+            sh_last = prev == static_cast<int>(CS) - 1;
+            if (sh_last) gbar[2] = 0;
+        }
+        __syncthreads();
+        pdl_trigger();  // every CTA of the grid is past its last barrier
+        if (!sh_last) return;
+        for (int x = t; x < static_cast<int>(CS) * HP * kPart; x += kLT) allp[x] = __ldcg(gp + x);
+        __syncthreads();
+        for (int x = t; x < HP * kD; x += kLT) {
+            const int h = x / kD, e = x - h * kD;
+            float M = -INFINITY;
+            for (unsigned c = 0; c < CS; ++c) M = fmaxf(M, allp[(c * HP + h) * kPart + kD]);
+            float Lsum = 0.f, O = 0.f;
+            for (unsigned c = 0; c < CS; ++c) {
+                const float* pc = allp + (c * HP + h) * kPart;
+                if (pc[kD] == -INFINITY) continue;
+                const float wgt = expf(pc[kD] - M);
+                Lsum += wgt * pc[kD + 1];
+                O += wgt * pc[e];
+            }
+            a.out[static_cast<int64_t>(m * HP + h) * kD + e] = O / Lsum;
+        }
+    } else {
+        // many CTAs per group: a barrier, then CTA r merges heads r, r + CS, ... with every
+        // CTA's partials of those heads staged ([local head][CS][kPart])
+        group_barrier(gbar, static_cast<int>(CS), gen);
+        pdl_trigger();
+        for (int h = rank, hl = 0; h < HP; h += CS, ++hl)
+            for (int x = t; x < static_cast<int>(CS) * kPart; x += kLT) {
+                const int c = x / kPart, o = x - c * kPart;
+                allp[(hl * CS + c) * kPart + o] = __ldcg(gp + (static_cast<size_t>(c) * HP + h) * kPart + o);
+            }
+        __syncthreads();
+        for (int h = rank, hl = 0; h < HP; h += CS, ++hl) {
             if (t < kD) {
                 float M = -INFINITY;
-                for (unsigned c = 0; c < CS; ++c) M = fmaxf(M, ld_dsmem(dsmem_addr(part + h * kPart + kD, c)));
+                for (unsigned c = 0; c < CS; ++c) M = fmaxf(M, allp[(hl * CS + c) * kPart + kD]);
                 float Lsum = 0.f, O = 0.f;
                 for (unsigned c = 0; c < CS; ++c) {
-                    const float mc_ = ld_dsmem(dsmem_addr(part + h * kPart + kD, c));
-                    if (mc_ == -INFINITY) continue;
-                    const float wgt = expf(mc_ - M);
-                    Lsum += wgt * ld_dsmem(dsmem_addr(part + h * kPart + kD + 1, c));
-                    O += wgt * ld_dsmem(dsmem_addr(part + h * kPart + t, c));
+                    const float* pc = allp + (hl * CS + c) * kPart;
+                    if (pc[kD] == -INFINITY) continue;
+                    const float wgt = expf(pc[kD] - M);
+                    Lsum += wgt * pc[kD + 1];
+                    O += wgt * pc[t];
                 }
                 a.out[static_cast<int64_t>(m * HP + h) * kD + t] = O / Lsum;
             }
         }
-    } else {
-        __syncthreads();
-        for (int x = t; x < HP * kPart; x += kLT) gp[static_cast<size_t>(rank) * HP * kPart + x] = part[x];
-        float* allp = reinterpret_cast<float*>(stage);  // staged partials (tiles are done)
-        if (static_cast<int>(CS) * HP * kPart * 4 <= kStageBytes) {
-            // the last CTA to finish (acq_rel ticket) merges every head: no CTA waits
-            __shared__ int sh_last;
-            __syncthreads();
-            if (t == 0) {
-                int prev;
-                asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(prev) : "l"(gbar + 2) : "memory");
-                sh_last = prev == static_cast<int>(CS) - 1;
-                if (sh_last) gbar[2] = 0;
-            }
-            __syncthreads();
-            pdl_trigger();
-            if (!sh_last) return;
-            for (int x = t; x < static_cast<int>(CS) * HP * kPart; x += kLT) allp[x] = __ldcg(gp + x);
-            __syncthreads();
-            for (int x = t; x < HP * kD; x += kLT) {
-                const int h = x / kD, e = x - h * kD;
-                float M = -INFINITY;
-                for (unsigned c = 0; c < CS; ++c) M = fmaxf(M, allp[(c * HP + h) * kPart + kD]);
-                float Lsum = 0.f, O = 0.f;
-                for (unsigned c = 0; c < CS; ++c) {
-                    const float* pc = allp + (c * HP + h) * kPart;
-                    if (pc[kD] == -INFINITY) continue;
-                    const float wgt = expf(pc[kD] - M);
-                    Lsum += wgt * pc[kD + 1];
-                    O += wgt * pc[e];
-                }
-                a.out[static_cast<int64_t>(m * HP + h) * kD + e] = O / Lsum;
-            }
-        } else {
-            // many CTAs per group: a barrier, then CTA r merges heads r, r + CS, ... with
-            // every CTA's partials of those heads staged ([local head][CS][kPart])
-            group_barrier(gbar, static_cast<int>(CS), gen);
-            pdl_trigger();
-            for (int h = rank, hl = 0; h < HP; h += CS, ++hl)
-                for (int x = t; x < static_cast<int>(CS) * kPart; x += kLT) {
-                    const int c = x / kPart, o = x - c * kPart;
-                    allp[(hl * CS + c) * kPart + o] = __ldcg(gp + (static_cast<size_t>(c) * HP + h) * kPart + o);
-                }
-            __syncthreads();
-            for (int h = rank, hl = 0; h < HP; h += CS, ++hl) {
-                if (t < kD) {
-                    float M = -INFINITY;
-                    for (unsigned c = 0; c < CS; ++c) M = fmaxf(M, allp[(hl * CS + c) * kPart + kD]);
-                    float Lsum = 0.f, O = 0.f;
-                    for (unsigned c = 0; c < CS; ++c) {
-                        const float* pc = allp + (hl * CS + c) * kPart;
-                        if (pc[kD] == -INFINITY) continue;
-                        const float wgt = expf(pc[kD] - M);
-                        Lsum += wgt * pc[kD + 1];
-                        O += wgt * pc[t];
-                    }
-                    a.out[static_cast<int64_t>(m * HP + h) * kD + t] = O / Lsum;
-                }
-            }
-        }
     }
     trace(20, 6);
-    if constexpr (CLU) cluster_sync_all();  // partials stay readable until every CTA has merged
-    trace(20, 7);
 }
 
-int g_cluster_override = -1;  // dev: 0 = grid mode, >0 = cluster mode of that size, -1 = default
-constexpr int kKeysMax = 16384;    // chunk keys per stage selection
-constexpr int kMaxGroupCtas = 160; // grid mode: CTAs per KV group
-
-template <int HP, bool CLU>
+template <int HP>
 cudaError_t launch_layer(const LayerParams& p, int ctas, size_t smem, cudaStream_t s) {
-    auto kern = decode_layer_kernel<HP, CLU>;
+    auto kern = decode_layer_kernel<HP>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    if (CLU && ctas > 8 && (e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess)
-        return e;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(ctas, p.a.n_masks);
     cfg.blockDim = dim3(kLT);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[2];
-    int na = 0;
-    if (CLU) {
-        attr[na].id = cudaLaunchAttributeClusterDimension;
-        attr[na].val.clusterDim.x = ctas;
-        attr[na].val.clusterDim.y = 1;
-        attr[na].val.clusterDim.z = 1;
-        ++na;
-    }
-    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[na].val.programmaticStreamSerializationAllowed = 1;
-    ++na;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = na;
+    cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kern, p);
 }
 
-template <bool CLU>
 cudaError_t dispatch(int hp, const LayerParams& p, int ctas, size_t smem, cudaStream_t s) {
     switch (hp) {
-        case 1: return launch_layer<1, CLU>(p, ctas, smem, s);
-        case 2: return launch_layer<2, CLU>(p, ctas, smem, s);
-        case 4: return launch_layer<4, CLU>(p, ctas, smem, s);
-        default: return launch_layer<8, CLU>(p, ctas, smem, s);
+        case 1: return launch_layer<1>(p, ctas, smem, s);
+        case 2: return launch_layer<2>(p, ctas, smem, s);
+        case 4: return launch_layer<4>(p, ctas, smem, s);
+        default: return launch_layer<8>(p, ctas, smem, s);
     }
 }
 
 size_t ws_stage_bytes(int32_t n_masks, int32_t max_chunks0) { return align_up(hp_decode_stage_workspace_bytes(n_masks, max_chunks0), 256); }
 size_t ws_keys_bytes(int32_t n_masks) { return align_up(static_cast<size_t>(2) * n_masks * kKeysMax * 4, 256); }
 size_t ws_part_bytes(int32_t n_masks) { return align_up(static_cast<size_t>(n_masks) * kMaxGroupCtas * 8 * kPart * 4, 256); }
-constexpr int kBarInts = 4;  // per mask: arrivals, generation, merge ticket, pad
 
 // host validation shared by _supported and the launch; returns HP_OK or sets the error
 int check_args(const hp_decode_layer_args& a) {
@@ -716,9 +677,9 @@ int check_args(const hp_decode_layer_args& a) {
 
 }  // namespace
 
-// stage-0 scores (hp_decode_stage's workspace), then the grid mode's exchanged keys,
-// attention partials and per-group barrier counters (which must start at zero: the
-// workspace must be zeroed once before first use; every launch leaves them at zero)
+// stage-0 scores (hp_decode_stage's workspace), then the exchanged keys, the attention
+// partials and per-group barrier counters (which must start at zero: the workspace must
+// be zeroed once before first use; every launch leaves them consistent for the next)
 extern "C" size_t hp_decode_layer_workspace_bytes(int32_t n_masks, int32_t max_chunks0) {
     return ws_stage_bytes(n_masks, max_chunks0) + ws_keys_bytes(n_masks) + ws_part_bytes(n_masks) +
            align_up(static_cast<size_t>(n_masks) * kBarInts * 4, 256);
@@ -726,22 +687,14 @@ extern "C" size_t hp_decode_layer_workspace_bytes(int32_t n_masks, int32_t max_c
 
 extern "C" int hp_decode_layer_supported(const hp_decode_layer_args* ap) {
     if (!ap) return 0;
-    const int rc = check_args(*ap);
-    if (rc != HP_OK) return 0;
-    return 1;
+    return check_args(*ap) == HP_OK ? 1 : 0;
 }
 
 #if defined(HP_TRACE) || defined(HP_DEV)  // developer hooks: dev builds only (include/hipprune_b200_dev.h)
-// dev build: per-CTA phase stamps of the layer kernel (trace id 20) into buf
+// per-CTA phase stamps of the layer kernel (trace ids 20-22) into buf
 extern "C" int hp_layer_trace_enable(unsigned long long* buf, int kernel_id) {
     if (int rc = hph::check_cuda(cudaMemcpyToSymbol(g_trace_buf, &buf, sizeof(buf)), "hp_layer_trace_enable")) return rc;
     return hph::check_cuda(cudaMemcpyToSymbol(g_trace_kernel, &kernel_id, sizeof(int)), "hp_layer_trace_enable");
-}
-
-// dev: cluster size override (0 = automatic)
-extern "C" int hp_decode_layer_cluster(int cs) {
-    g_cluster_override = cs;  // <= 0: grid mode
-    return HP_OK;
 }
 #endif
 
@@ -756,7 +709,7 @@ extern "C" int hp_decode_layer(const hp_decode_layer_args* ap, void* stream) {
     const int64_t n0 = std::max<int64_t>(0, upper - a.sink_tokens);
     const int lc0 = a.chunk_size[0];
     const int32_t mc0 = static_cast<int32_t>(std::max<int64_t>(1, (n0 + lc0 - 1) / lc0));
-    if (mc0 > 16384) return hph::set_error(HP_INVALID_ARGUMENT, "hp_decode_layer: %d stage-0 chunks exceed 16384", mc0);
+    if (mc0 > kKeysMax) return hph::set_error(HP_INVALID_ARGUMENT, "hp_decode_layer: %d stage-0 chunks exceed %d", mc0, kKeysMax);
     const size_t need = hp_decode_layer_workspace_bytes(a.n_masks, mc0);
     if (!a.workspace || a.workspace_bytes < need) return hph::set_error(HP_INVALID_ARGUMENT, "hp_decode_layer: workspace too small");
     if (a.n_masks > 4096) return hph::set_error(HP_INVALID_ARGUMENT, "hp_decode_layer: at most 4096 masks");
@@ -768,7 +721,7 @@ extern "C" int hp_decode_layer(const hp_decode_layer_args* ap, void* stream) {
     p.scores0 = reinterpret_cast<const float*>(static_cast<const char*>(a.workspace) + align_up(static_cast<size_t>(a.n_masks) * 4, 256));
     const bool sel0 = a.refresh[0] && !(n0 <= a.keep[0] || mc0 <= a.keep[0] / lc0);
     if (sel0) {
-        // stage 0's descent on its own kernel (decode.cu): scores only, selected in the cluster
+        // stage 0's descent on its own kernel (decode.cu): scores only, selected in the layer kernel
         hp_decode_stage_args sa{};
         sa.chunk_size = lc0;
         sa.keep = a.keep[0];
@@ -795,16 +748,14 @@ extern "C" int hp_decode_layer(const hp_decode_layer_args* ap, void* stream) {
         p.planes0 = variant == HP_STAGE_WIDE ? a.heads_per_mask : 1;
         if (int rc = hp_decode_stage(&sa, stream)) return rc;
     }
-    // per-stage input bounds -> shared-memory sizing
-    int64_t bound = n0;
-    int keys_cap = 1, red_cap = 32, sel_total = 0;
-    // grid mode (default): one co-resident CTA per SM, n_SM / n_masks CTAs per KV group
-    const bool cluster_mode = g_cluster_override > 0;
+    // one co-resident CTA per SM, n_SM / n_masks CTAs per KV group
     int dev = 0, n_sm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     const int ctas = std::max(1, std::min(kMaxGroupCtas, n_sm / std::max(1, a.n_masks)));
-    const int cs = cluster_mode ? g_cluster_override : ctas;
+    // per-stage input bounds -> shared-memory sizing
+    int64_t bound = n0;
+    int keys_cap = 1, red_cap = 32, sel_total = 0;
     for (int i = 0; i < a.n_stages; ++i) {
         if (i > 0) bound = a.refresh[i - 1] ? std::min<int64_t>(bound, a.keep[i - 1]) : a.keep[i - 1];
         const int lc = a.chunk_size[i];
@@ -813,7 +764,7 @@ extern "C" int hp_decode_layer(const hp_decode_layer_args* ap, void* stream) {
         sel_total += std::max(1, a.keep[i] / lc);
         if (a.refresh[i]) {
             keys_cap = static_cast<int>(std::max<int64_t>(keys_cap, cc));
-            const int64_t gpc = ((cc + 31) / 32 + cs - 1) / cs;
+            const int64_t gpc = ((cc + 31) / 32 + ctas - 1) / ctas;
             red_cap = static_cast<int>(std::max<int64_t>(red_cap, gpc * 32));
         }
     }
@@ -828,13 +779,9 @@ extern "C" int hp_decode_layer(const hp_decode_layer_args* ap, void* stream) {
     p.gpart = reinterpret_cast<float*>(ws + off);
     off += ws_part_bytes(a.n_masks);
     p.gbar = reinterpret_cast<int*>(ws + off);
-    const LayerSmem L(p.keys_cap, sel_total, a.heads_per_mask, red_cap, cluster_mode ? 2 : 1);
-    cudaError_t e;
-    if (cluster_mode) {
-        e = dispatch<true>(a.heads_per_mask, p, cs, L.bytes, s);
-    } else {
-        e = dispatch<false>(a.heads_per_mask, p, ctas, L.bytes, s);
-    }
+    const LayerSmem L(sel_total, a.heads_per_mask, red_cap);
+    if (L.bytes + 8 * 1024 > 227 * 1024) return hph::set_error(HP_INVALID_ARGUMENT, "hp_decode_layer: stage lists too long for shared memory");
+    const cudaError_t e = dispatch(a.heads_per_mask, p, ctas, L.bytes, s);
     if (e != cudaSuccess) return hph::check_cuda(e, "decode_layer_kernel");
     return hph::check_cuda(cudaGetLastError(), "decode_layer_kernel");
 }

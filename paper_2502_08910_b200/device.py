@@ -575,10 +575,10 @@ class FusedDecodeLayer:
         refresh = list(refresh) if refresh is not None else [True] * S
         if self._fused is None:
             self._fused = self.fused_supported()
-        # hp_decode_layer when a stage with a successor stage is due (its selection and the
-        # next stage chain inside one kernel); steps that only rescore the last stage or reuse
-        # every cache run the per-stage kernels, measured faster there
-        if self._fused and (self._fused == "always" or any(refresh[:-1])):
+        # hp_decode_layer when any stage is due (the stages' selections and the attention
+        # chain inside one kernel); a step that reuses every cache runs the split-K BSA
+        # kernel alone, measured faster for that step
+        if self._fused and (self._fused == "always" or any(refresh)):
             return self._run_fused(t, refresh, stream, materialize, mat_stream)
         pos = t - 1
         upper = t - self.stream_tokens if t > self.stream_tokens else 0

@@ -94,6 +94,5 @@ def test_product_library_has_no_dev_hooks():
     if not _capi.LIB_PATH.exists() or "trace" in _capi.LIB_PATH.name or "HP_LIB" in __import__("os").environ:
         pytest.skip("product library not built / a dev build is selected")
     L = ctypes.CDLL(str(_capi.LIB_PATH))
-    for name in ("hp_trace_enable", "hp_layer_trace_enable", "hp_debug_cut", "hp_debug_prefill_progress",
-                 "hp_decode_layer_cluster"):
+    for name in ("hp_trace_enable", "hp_layer_trace_enable", "hp_debug_cut", "hp_debug_prefill_progress"):
         assert not hasattr(L, name), name
