@@ -1260,10 +1260,13 @@ int stage_variant(const hp_decode_stage_args& a, size_t elem) {
     const int hpm = a.heads_per_mask;
     const int groups = (a.max_chunks + 31) / 32;
     const int64_t wide_items = static_cast<int64_t>(a.n_masks) * groups * hpm;
+    // from half a wave of descents up the stage is bandwidth-bound and the one-wave kernel
+    // (1.0x bytes) beats the lookahead kernel (1.33x); below it the halved round count
+    // wins (measured at 1M: 4 groups 32.6 vs 41.2 us; 2 groups 24.1 vs 21.7; 1 group 22.1 vs 18.2)
     if (a.scores_out == nullptr && a.chunk_size > 8 && hpm <= 8 &&
         align_up(static_cast<size_t>(a.n_masks) * 4, 256) + static_cast<size_t>(a.n_masks) * hpm * a.max_chunks * 4 <=
             a.workspace_bytes &&
-        wide_items > 2048)
+        wide_items >= 2048)
         return HP_STAGE_WIDE;
     if (a.chunk_size <= 8 && 32 % a.chunk_size == 0 && (a.n_q_heads / a.keys.n_kv) % hpm == 0)
         return HP_STAGE_ALLROWS;
