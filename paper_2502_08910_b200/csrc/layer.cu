@@ -109,27 +109,19 @@ __device__ __forceinline__ void ldmatrix_x4_trans(uint32_t* r, const void* p) {
                  : "r"(smem_u32(p)));
 }
 
-// Group barrier over the n CTAs of one KV group, sense-reversing: bar[0] counts
-// arrivals, bar[1] is the generation. Each CTA read the generation once at kernel start
-// (tracked locally after that); it arrives (acq_rel), the last arrival zeroes the count
-// and publishes gen + 1 (release), the others spin (acquire) until it appears. The
-// count is back at 0 after every barrier, so consecutive launches need no reset.
-__device__ __forceinline__ void group_barrier(int* bar, int n, int& gen) {
+// Group barrier over the CTAs of one KV group: each CTA arrives with a fire-and-forget
+// release add on a per-group counter and spins (acquire loads) until it reaches this
+// barrier's target — n per barrier, the counter starting each launch at 0 (the last CTA
+// to leave resets it). One L2 trip per arrival, no returned atomic on the critical path.
+__device__ __forceinline__ void group_barrier(int* ctr, int target) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        int prev;
-        asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(prev) : "l"(bar) : "memory");
-        if (prev == n - 1) {
-            asm volatile("st.relaxed.gpu.global.s32 [%0], 0;" ::"l"(bar) : "memory");
-            asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(bar + 1), "r"(gen + 1) : "memory");
-        } else {
-            int g2;
-            do {
-                asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(g2) : "l"(bar + 1) : "memory");
-            } while (g2 == gen);
-        }
+        asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(ctr) : "memory");
+        int v;
+        do {
+            asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+        } while (v < target);
     }
-    ++gen;
     __syncthreads();
 }
 
@@ -155,13 +147,11 @@ __global__ void __launch_bounds__(kLT, 1) decode_layer_kernel(const LayerParams 
     float* red = reinterpret_cast<float*>(smem + L.red);
     float* part = reinterpret_cast<float*>(smem + L.part);
     const int kvh = (m * HP) / (a.n_q_heads / a.kv.n_kv);  // the mask's heads share one kv head (host-checked)
-    int* gbar = P.gbar + kBarInts * m;
-    int gen = 0;
+    int* gbar = P.gbar + kBarInts * m;  // [0] barrier arrivals, [2] merge ticket, [3] exit ticket
+    int n_bar = 0;
 
     trace(20, 0);
     pdl_wait();
-    if (t == 0) asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(gen) : "l"(gbar + 1) : "memory");
-    gen = __shfl_sync(0xffffffffu, gen, 0);  // this launch's starting generation (no barrier completes before we arrive)
     bool safe = true;
     for (int i = t; i < HP * kD; i += kLT) {
         const float x = a.q[static_cast<int64_t>(m * HP) * kD + i];
@@ -374,7 +364,7 @@ __global__ void __launch_bounds__(kLT, 1) decode_layer_kernel(const LayerParams 
                 }
             }
             if (i == 1) trace(22, 1);
-            group_barrier(gbar, static_cast<int>(CS), gen);  // every CTA's keys are in L2
+            group_barrier(gbar, static_cast<int>(++n_bar * CS));  // every CTA's keys are in L2
             if (i == 1) trace(22, 2);
             const uint32_t* gk = P.gkeys + (static_cast<size_t>(buf) * a.n_masks + m) * P.keys_cap;
             for (int64_t j0 = 0; j0 < cc; j0 += 8 * kLT) {  // 8 independent loads in flight per thread
@@ -574,7 +564,10 @@ __global__ void __launch_bounds__(kLT, 1) decode_layer_kernel(const LayerParams 
             int prev;
             asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(prev) : "l"(gbar + 2) : "memory");
             sh_last = prev == static_cast<int>(CS) - 1;
-            if (sh_last) gbar[2] = 0;
+            if (sh_last) {  // every CTA is past every barrier: reset for the next launch
+                gbar[0] = 0;
+                gbar[2] = 0;
+            }
         }
         __syncthreads();
         pdl_trigger();  // every CTA of the grid is past its last barrier
@@ -598,7 +591,7 @@ __global__ void __launch_bounds__(kLT, 1) decode_layer_kernel(const LayerParams 
     } else {
         // many CTAs per group: a barrier, then CTA r merges heads r, r + CS, ... with every
         // CTA's partials of those heads staged ([local head][CS][kPart])
-        group_barrier(gbar, static_cast<int>(CS), gen);
+        group_barrier(gbar, static_cast<int>(++n_bar * CS));
         pdl_trigger();
         for (int h = rank, hl = 0; h < HP; h += CS, ++hl)
             for (int x = t; x < static_cast<int>(CS) * kPart; x += kLT) {
@@ -619,6 +612,15 @@ __global__ void __launch_bounds__(kLT, 1) decode_layer_kernel(const LayerParams 
                     O += wgt * pc[t];
                 }
                 a.out[static_cast<int64_t>(m * HP + h) * kD + t] = O / Lsum;
+            }
+        }
+        __syncthreads();
+        if (t == 0) {  // exit ticket: the last CTA out resets the counters for the next launch
+            int prev;
+            asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(prev) : "l"(gbar + 3) : "memory");
+            if (prev == static_cast<int>(CS) - 1) {
+                gbar[0] = 0;
+                gbar[3] = 0;
             }
         }
     }
