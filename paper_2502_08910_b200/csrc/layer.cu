@@ -572,7 +572,22 @@ __global__ void __launch_bounds__(kLT, 1) decode_layer_kernel(const LayerParams 
         __syncthreads();
         pdl_trigger();  // every CTA of the grid is past its last barrier
         if (!sh_last) return;
-        for (int x = t; x < static_cast<int>(CS) * HP * kPart; x += kLT) allp[x] = __ldcg(gp + x);
+        {
+            const int n = static_cast<int>(CS) * HP * kPart;
+            for (int x0 = 0; x0 < n; x0 += 8 * kLT) {  // 8 independent L2 loads in flight per thread
+                float v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int x = x0 + u * kLT + t;
+                    v[u] = x < n ? __ldcg(gp + x) : 0.f;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int x = x0 + u * kLT + t;
+                    if (x < n) allp[x] = v[u];
+                }
+            }
+        }
         __syncthreads();
         for (int x = t; x < HP * kD; x += kLT) {
             const int h = x / kD, e = x - h * kD;

@@ -18,7 +18,10 @@ del k, v
 layer = D.FusedDecodeLayer(kv, stages, sink=256, stream_tokens=1024, n_q_heads=groups * hpm, n_masks=groups)
 layer.q.copy_(q.view(layer.q.shape))
 L = _capi.lib()
-L.hp_layer_trace_enable.argtypes = [C.c_void_p, C.c_int]
+import os
+# decode.cu kernels (ids < 20) trace through hp_trace_enable, the layer kernel through its own
+_en = L.hp_trace_enable if int(os.environ.get("KID", "20")) < 20 else L.hp_layer_trace_enable
+_en.argtypes = [C.c_void_p, C.c_int]
 buf = torch.zeros((16384, 8), dtype=torch.int64, device="cuda")
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 for _ in range(3):
@@ -29,16 +32,19 @@ kid = int(os.environ.get("KID", "20"))
 for name, fl in {"full": [True] * 3, "s23": [False, True, True], "s3": [False, False, True], "bsa": [False] * 3}.items():
     for rep in range(2):
         buf.zero_()
-        _capi.check(L.hp_layer_trace_enable(buf.data_ptr(), kid))
+        _capi.check(_en(buf.data_ptr(), kid))
         flush.zero_()
         torch.cuda.synchronize()
         layer.run(t, refresh=fl, materialize=False)
         torch.cuda.synchronize()
-        _capi.check(L.hp_layer_trace_enable(None, -1))
+        _capi.check(_en(None, -1))
     ball = buf.cpu().numpy().astype(np.float64)
     used = ball[:8192, 0] > 0
     b = ball[:8192][used]
     ck = ball[8192:][used]
+    if not len(b):
+        print(f"== {name}: no CTA recorded trace {kid}")
+        continue
     t0 = b[:, 0].min()
     rel = np.where(b > 0, (b - t0) / 1000.0, np.nan)
     crel = np.where(b > 0, ck - ck[:, :1], np.nan)  # cycles since the CTA's slot 0 (same SM)
