@@ -142,6 +142,14 @@ typedef struct hp_stage_args {
 size_t hp_stage_workspace_bytes(int32_t n_lists, int32_t max_chunks, int32_t keep, int32_t chunk_size);
 int hp_prune_stage(const hp_stage_args* args, void* stream);
 
+/* Which descent hp_prune_stage launches (host-only query, no launch): query-block stages
+ * (16..64 q rows, <= 8 heads per mask) over bf16 keys with the keys_exact flag, d = 128, RoPE off,
+ * score rows on the tensor cores with a certified error bound and settle every undecided
+ * comparison and the top-K boundary with exact dots; everything else runs the CUDA-core
+ * descent. Both give the reference's indices. */
+enum hp_prune_variant { HP_PRUNE_CUDA_CORE = 0, HP_PRUNE_TENSOR_CORE = 1 };
+int hp_prune_stage_variant(const hp_stage_args* args, int32_t* variant);
+
 /* Sub-block remap between stages with different b_q (pruning.cpp:285-303):
  * next(m2) = { idx in parent(min(m2/ratio, nb-1)) : idx < middle_upper(bq_next, m2) }. */
 int hp_remap_blocks(const int32_t* in_list, const int32_t* in_count, int64_t in_stride,

@@ -20,6 +20,7 @@ HP_OK = 0
 HP_F32, HP_BF16 = 0, 1
 HP_ROPE_CHUNK_INDEXED, HP_ROPE_RELATIVE, HP_ROPE_STREAMING = 0, 1, 2
 STAGE_VARIANTS = {0: "classic", 1: "lookahead", 2: "wide", 3: "allrows"}  # hp_stage_variant
+PRUNE_VARIANTS = {0: "cuda_core", 1: "tensor_core"}  # hp_prune_variant
 BSA_VARIANTS = {0: "ticket", 1: "cluster"}  # hp_bsa_variant
 
 
@@ -135,7 +136,7 @@ _lib = None
 
 # every symbol include/hipprune_b200.h declares
 EXPORTS = ["hp_last_error", "hp_version", "hp_device_available", "hp_build_rope_table",
-           "hp_stage_workspace_bytes", "hp_prune_stage", "hp_remap_blocks",
+           "hp_stage_workspace_bytes", "hp_prune_stage", "hp_prune_stage_variant", "hp_remap_blocks",
            "hp_selected_indices", "hp_bsa_workspace_bytes", "hp_bsa", "hp_lse_merge",
            "hp_decode_stage_workspace_bytes", "hp_decode_stage", "hp_decode_bsa_workspace_bytes",
            "hp_decode_bsa", "hp_decode_stage_variant", "hp_decode_bsa_variant",
@@ -162,6 +163,8 @@ def lib():
     L.hp_stage_workspace_bytes.argtypes = [C.c_int32] * 4
     L.hp_prune_stage.restype = C.c_int
     L.hp_prune_stage.argtypes = [C.POINTER(StageArgs), C.c_void_p]
+    L.hp_prune_stage_variant.restype = C.c_int
+    L.hp_prune_stage_variant.argtypes = [C.POINTER(StageArgs), C.POINTER(C.c_int32)]
     L.hp_remap_blocks.restype = C.c_int
     L.hp_remap_blocks.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32,
                                   C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_int32,

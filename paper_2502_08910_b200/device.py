@@ -17,6 +17,7 @@ Mapping to the reference (paths relative to /root/reference/proj):
 """
 from __future__ import annotations
 
+import collections
 import ctypes as C
 import math
 from dataclasses import dataclass
@@ -204,7 +205,14 @@ def prune_stage(stage, q: torch.Tensor, kv: PagedKV, *, n_masks: int, n_blocks: 
                   out_count=_ptr(out_count), out_stride=out_list.shape[-1], workspace=_ptr(w),
                   workspace_bytes=w.numel(), keys=kv.view(), rope=policy.ctx(layer1, rope),
                   keys_exact=_ptr(getattr(kv, "keys_exact", None)))
+    v = C.c_int32(-1)
+    check(lib().hp_prune_stage_variant(C.byref(a), C.byref(v)))
+    PRUNE_VARIANTS_USED.append(v.value)
     check(lib().hp_prune_stage(C.byref(a), C.c_void_p(_stream(stream))))
+
+
+# descent kernel of the recent prune_stage calls (hp_prune_variant), for tests and tools
+PRUNE_VARIANTS_USED: collections.deque = collections.deque(maxlen=1024)
 
 
 def build_mask(q: torch.Tensor, kv: PagedKV, stages, *, sink: int, stream_tokens: int,

@@ -80,7 +80,9 @@ def test_prefill_mask_and_tc_vs_oracle(port, t_kv, t_q, stages, sink, stream):
     groups, hpm = 2, 4
     q, k, v = synth.generate(groups * hpm, groups, t_kv, 128, t_q=t_q, seed=5)
     kv = D.PagedKV(k, v, page_size=64)
+    D.PRUNE_VARIANTS_USED.clear()
     lists, counts, _, bs, off = D.build_mask(q, kv, stages, sink=sink, stream_tokens=stream, n_masks=groups)
+    assert set(D.PRUNE_VARIANTS_USED) == {1}  # every stage on the tensor-core descent
     got = D.bsa_prefill_tc(q, kv, lists, counts, block_size=bs, query_offset=off, sink=sink, stream_tokens=stream)
     torch.cuda.synchronize()
     qh, kh, vh = q.cpu().numpy(), k.float().cpu().numpy(), v.float().cpu().numpy()
@@ -98,3 +100,86 @@ def test_prefill_mask_and_tc_vs_oracle(port, t_kv, t_q, stages, sink, stream):
         og = g_out[g * hpm:(g + 1) * hpm].astype(np.float64)
         err = np.abs(og - want).max() / np.abs(want).max()
         assert err <= BF16_RTOL, (g, err)
+
+
+def _masks_vs_oracle(port, D, q, k, stages, sink, stream, groups, hpm):
+    kv = D.PagedKV(k, k, page_size=64)
+    lists, counts, _, bs, off = D.build_mask(q, kv, stages, sink=sink, stream_tokens=stream, n_masks=groups)
+    torch.cuda.synchronize()
+    qh, kh = q.cpu().numpy(), k.float().cpu().numpy()
+    L, Cn = lists.cpu().numpy(), counts.cpu().numpy()
+    for g in range(groups):
+        want_lists, _, wbs, woff = port.build_mask(qh[g * hpm:(g + 1) * hpm], kh[g:g + 1], stages,
+                                                   sink=sink, stream=stream, threads=8)
+        assert (wbs, woff) == (bs, off)
+        for b, wl in enumerate(want_lists):
+            assert np.array_equal(L[g, b, : Cn[g, b]], wl), (g, b)
+
+
+@pytest.mark.parametrize("period", [97, 5])
+def test_tc_descent_near_ties_exact(port, period):
+    """The tensor-core descent's certified comparisons and top-K boundary under massive
+    ties: keys repeat with a short period, so most branch comparisons and most chunk
+    scores are exactly equal (every one undecided by the bound) — the exact re-decisions
+    and the boundary replay must still give the reference's lists (strict '>', lowest
+    chunk index first)."""
+    D = _D()
+    from paper_2502_08910_b200 import synth
+    groups, hpm, t_kv, t_q = 2, 4, 8192, 512
+    stages = [(64, 64, 2048), (64, 16, 512), (64, 4, 256)]
+    q, k, _ = synth.generate(groups * hpm, groups, t_kv, 128, t_q=t_q, seed=21)
+    idx = torch.arange(t_kv, device=k.device) % period
+    k = k[:, idx].contiguous()
+    D.PRUNE_VARIANTS_USED.clear()
+    _masks_vs_oracle(port, D, q, k, stages, 256, 1024, groups, hpm)
+    assert set(D.PRUNE_VARIANTS_USED) == {1}
+
+
+def test_tc_descent_mixed_precision_heads(port):
+    """One head's q rows are not bf16-exact: that head's CTAs score with the separately
+    rounded fp32 dots, the others on the tensor cores, and the boundary replay uses each
+    head's own exact arithmetic."""
+    D = _D()
+    from paper_2502_08910_b200 import synth
+    groups, hpm, t_kv, t_q = 2, 4, 8192, 512
+    stages = [(64, 64, 2048), (64, 16, 512), (64, 4, 256)]
+    q, k, _ = synth.generate(groups * hpm, groups, t_kv, 128, t_q=t_q, seed=23)
+    q[1] += 1e-3 * torch.randn_like(q[1])  # head 1 (group 0) in full fp32
+    _masks_vs_oracle(port, D, q, k, stages, 256, 1024, groups, hpm)
+
+
+_C4_MASKS = """
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+from paper_2502_08910_b200 import device as D, synth
+q, k, v = synth.generate(32, 8, 1 << 17, 128, t_q=1 << 15, seed=11)
+kv = D.PagedKV(k, v, page_size=64)
+lists, counts, _, bs, off = D.build_mask(q, kv, [(64, 256, 32768), (64, 32, 8192), (64, 8, 2048)],
+                                         sink=256, stream_tokens=1024, n_masks=8)
+np.savez({out!r}, lists=lists.cpu().numpy(), counts=counts.cpu().numpy(),
+         variants=np.array(list(D.PRUNE_VARIANTS_USED)))
+"""
+
+
+def test_tc_descent_equals_cuda_core_at_c4(tmp_path):
+    """C4 size (a 32K-row chunk at 128K, 8 KV groups, the 3k preset): every list of the
+    tensor-core build_mask equals the CUDA-core descent's (HP_TC_DESCENT=0, itself
+    index-exact against the oracle) — two independent exact paths at full size."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = str(Path(__file__).resolve().parents[1])
+    res = {}
+    for name, env in (("tc", "1"), ("cc", "0")):
+        out = str(tmp_path / f"{name}.npz")
+        subprocess.run([sys.executable, "-c", _C4_MASKS.format(root=root, out=out)], check=True,
+                       env={**os.environ, "HP_TC_DESCENT": env}, timeout=600)
+        res[name] = np.load(out)
+    assert set(res["tc"]["variants"]) == {1} and set(res["cc"]["variants"]) == {0}
+    assert np.array_equal(res["tc"]["counts"], res["cc"]["counts"])
+    c = res["tc"]["counts"]
+    lt, lc = res["tc"]["lists"], res["cc"]["lists"]
+    for g in range(c.shape[0]):
+        for b in range(c.shape[1]):
+            assert np.array_equal(lt[g, b, : c[g, b]], lc[g, b, : c[g, b]]), (g, b)
