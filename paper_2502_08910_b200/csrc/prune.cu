@@ -354,6 +354,7 @@ constexpr int kTcWarps = 8;
 constexpr int kTcQBytes = 64 * 128 * 4;       // fp32 q rows (fallback) or padded bf16 q rows
 constexpr size_t kTcSmem = kTcQBytes + static_cast<size_t>(kTcWarps) * 32 * kTcRow;
 constexpr float kTcBound = 1.0f / 32768.0f;   // 2^-15
+constexpr int kTcMaxHeads = 8;                // heads per mask on this path (rep offsets per chunk)
 
 __device__ __forceinline__ void ldsm_x4(uint32_t* r, uint32_t addr) {
     asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -373,27 +374,30 @@ __device__ __forceinline__ void mma16816(float* c, const uint32_t* a, uint32_t b
 __device__ __forceinline__ float tc_sigma(uint32_t ks, uint32_t qa, int rows, int lane) {
     const int tq = lane & 3, mi = lane >> 3, r8 = lane & 7;
     float mx[2][2] = {{-INFINITY, -INFINITY}, {-INFINITY, -INFINITY}};
-#pragma unroll 1
-    for (int mt = 0; mt < 2; ++mt) {  // one 16-key m-tile at a time (its A fragments in registers)
-        uint32_t a[8][4];
+    uint32_t a[2][8][4];  // both m-tiles' A fragments: every B fragment feeds two MMAs
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
         for (int k = 0; k < 8; ++k)
-            ldsm_x4(a[k], ks + (mt * 16 + (mi & 1) * 8 + r8) * kTcRow + (k * 16 + (mi >> 1) * 8) * 2);
+            ldsm_x4(a[mt][k], ks + (mt * 16 + (mi & 1) * 8 + r8) * kTcRow + (k * 16 + (mi >> 1) * 8) * 2);
 #pragma unroll 1
-        for (int nt = 0; nt * 8 < rows; ++nt) {
-            float c[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int nt = 0; nt * 8 < rows; ++nt) {
+        float c[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
 #pragma unroll
-            for (int kp = 0; kp < 4; ++kp) {
-                uint32_t b[4];
-                ldsm_x4(b, qa + (nt * 8 + r8) * kTcRow + ((2 * kp + (mi >> 1)) * 16 + (mi & 1) * 8) * 2);
-                mma16816(c, a[2 * kp], b[0], b[1]);
-                mma16816(c, a[2 * kp + 1], b[2], b[3]);
+        for (int kp = 0; kp < 4; ++kp) {
+            uint32_t b[4];
+            ldsm_x4(b, qa + (nt * 8 + r8) * kTcRow + ((2 * kp + (mi >> 1)) * 16 + (mi & 1) * 8) * 2);
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt) {
+                mma16816(c[mt], a[mt][2 * kp], b[0], b[1]);
+                mma16816(c[mt], a[mt][2 * kp + 1], b[2], b[3]);
             }
-            const bool v0 = nt * 8 + 2 * tq < rows, v1 = nt * 8 + 2 * tq + 1 < rows;
-            const float y0 = fmaxf(v0 ? c[0] : -INFINITY, v1 ? c[1] : -INFINITY);
-            const float y1 = fmaxf(v0 ? c[2] : -INFINITY, v1 ? c[3] : -INFINITY);
-            if (mt == 0) { mx[0][0] = fmaxf(mx[0][0], y0); mx[0][1] = fmaxf(mx[0][1], y1); }
-            else { mx[1][0] = fmaxf(mx[1][0], y0); mx[1][1] = fmaxf(mx[1][1], y1); }
+        }
+        const bool v0 = nt * 8 + 2 * tq < rows, v1 = nt * 8 + 2 * tq + 1 < rows;
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+            mx[mt][0] = fmaxf(mx[mt][0], fmaxf(v0 ? c[mt][0] : -INFINITY, v1 ? c[mt][1] : -INFINITY));
+            mx[mt][1] = fmaxf(mx[mt][1], fmaxf(v0 ? c[mt][2] : -INFINITY, v1 ? c[mt][3] : -INFINITY));
         }
     }
 #pragma unroll
@@ -475,7 +479,8 @@ __device__ __forceinline__ float row_norm_up(const unsigned char* krow) {
 }
 
 __global__ void __launch_bounds__(kTcWarps * 32, 2) prune_descent_tc_kernel(const hp_stage_args a, uint32_t* keys_out,
-                                                                          uint32_t* list_bound, int max_chunks) {
+                                                                          uint32_t* list_bound, uint16_t* rep_out,
+                                                                          int max_chunks) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int hpm = a.heads_per_mask;
     const int mb = blockIdx.z, hh = blockIdx.y;
@@ -618,6 +623,7 @@ __global__ void __launch_bounds__(kTcWarps * 32, 2) prune_descent_tc_kernel(cons
     // certifies the kept set and replays the chunks near its boundary exactly
     if (active) {
         atomicMax(keys_out + static_cast<int64_t>(mb) * max_chunks + j, order_key(s1));  // max over heads (pruning.cpp:182)
+        rep_out[(static_cast<int64_t>(mb) * max_chunks + j) * kTcMaxHeads + hh] = static_cast<uint16_t>(first - 1);
         if (a.path_out) a.path_out[(static_cast<int64_t>(mb) * max_chunks + j) * hpm + hh] = path;
     }
     float eb = active ? e1 : 0.f;
@@ -673,26 +679,18 @@ __device__ __forceinline__ float key_to_float(uint32_t u) {
 // Settle the approximate chunk keys of one list around the approximate K-th value T:
 // keys more than `band` above T are certainly kept (their exact score exceeds the exact
 // K-th), keys more than `band` below certainly dropped; the chunks in between have every
-// head's descent replayed with exact dots (rare: the band is ~1e-4 of the score scale)
-// and take their exact key. Kept / dropped become the extreme keys so the second select
+// head's representative (recorded by the descent, whose branch decisions are exact)
+// scored with exact dots (rare: the band is ~1e-4 of the score scale) and take their
+// exact key. Kept / dropped become the extreme keys so the second select
 // returns exactly the reference's set (pruning.cpp:170-192).
 __device__ void refine_band(const hp_stage_args& a, int mb, float* scw, int64_t cc, float T, float band,
-                            uint32_t fallback_heads, uint32_t* qstage, int* scan_tmp) {
+                            uint32_t fallback_heads, const uint16_t* reps, int max_chunks, int* scan_tmp) {
     uint32_t* kw = reinterpret_cast<uint32_t*>(scw);
     __shared__ int idx[kTopkThreads];
     __shared__ uint32_t xkey[kTopkThreads];
     const int hpm = a.heads_per_mask, m = mb / a.n_blocks, b = mb % a.n_blocks;
     const int r0 = b * a.query_block, rows = min(a.query_block, a.q_rows - r0);
     const int lane = threadIdx.x & 31, w = warp_id(), nw = blockDim.x >> 5;
-    // the FHFMA heads' q rows as padded bf16 words (the layout exact_sigma_warp reads)
-    for (int i = threadIdx.x; i < hpm * rows * 64; i += blockDim.x) {
-        const int h = i / (rows * 64), rem = i - h * rows * 64, t = rem >> 6, e = rem & 63;
-        if (fallback_heads >> h & 1u) continue;
-        const float2 x = *reinterpret_cast<const float2*>(
-            a.q + (static_cast<int64_t>(m * hpm + h) * a.q_rows + r0 + t) * 128 + 2 * e);
-        qstage[(h * 64 + t) * (kTcRow / 4) + e] = (__float_as_uint(x.x) >> 16) | (__float_as_uint(x.y) & 0xffff0000u);
-    }
-    const int64_t n_in = a.in_count[mb];
     const int lc = a.chunk_size;
     for (int64_t tile = 0; tile < cc; tile += blockDim.x) {
         const int64_t jj = tile + threadIdx.x;
@@ -710,26 +708,17 @@ __device__ void refine_band(const hp_stage_args& a, int mb, float* scw, int64_t 
         for (int task = w; task < n_band * hpm; task += nw) {  // (chunk, head) descents, one per warp
             const int e = task / hpm, h = task - e * hpm;
             const int64_t j = idx[e], base = j * lc;
-            const int len = static_cast<int>(min64(lc, n_in - base));
             const int qh = m * hpm + h;
             const int kv = qh / (a.n_q_heads / a.keys.n_kv);
             const bool fb = fallback_heads >> h & 1u;
-            const float* qg = a.q + (static_cast<int64_t>(qh) * a.q_rows + r0) * 128;
-            const uint32_t* qw = qstage + h * 64 * (kTcRow / 4);
+            const float* qg = a.q + (static_cast<int64_t>(qh) * a.q_rows + r0) * 128;  // L1-resident after the first row
             auto sigma = [&](int i) {
                 const unsigned char* row = reinterpret_cast<const unsigned char*>(
                     kv_row_ptr(a.keys, a.keys.k_pool, a.keys.k_host, kv, list_token(a, mb, base + i), 2));
-                return fb ? exact_sigma_gq(row, qg, rows, lane, false) : exact_sigma_warp(row, qw, rows, lane);
+                return exact_sigma_gq(row, qg, rows, lane, !fb);
             };
-            int iters = 0;
-            while ((1 << iters) < len) ++iters;
-            int first = 1, last = len;
-            float s1 = sigma(0);
-            for (int it = 0; it < iters && first < last; ++it) {  // Alg. 3 (pruning.cpp:69-98)
-                const int mid = (first + last + 1) >> 1;
-                const float m2 = sigma(mid - 1);
-                if (m2 > s1) { first = mid; s1 = m2; } else { last = mid - 1; }
-            }
+            // the representative's exact score (its branch decisions were already exact)
+            const float s1 = sigma(reps[(static_cast<int64_t>(mb) * max_chunks + j) * kTcMaxHeads + h]);
             if (lane == 0) atomicMax(&xkey[e], order_key(s1));  // max over heads (pruning.cpp:182)
         }
         __syncthreads();
@@ -739,11 +728,11 @@ __device__ void refine_band(const hp_stage_args& a, int mb, float* scw, int64_t 
 }
 
 // Exact top-(k/l_c) chunk selection + ordered emission of the survivors.
-__global__ void __launch_bounds__(kTopkThreads) prune_topk_kernel(const hp_stage_args a,
+__global__ void __launch_bounds__(kTopkThreads, 2) prune_topk_kernel(const hp_stage_args a,
                                                                   const float* scores,
                                                                   int32_t* sel_ws, int max_chunks,
                                                                   int kmax, int* status, bool keyed,
-                                                                  const uint32_t* list_bound) {
+                                                                  const uint32_t* list_bound, const uint16_t* reps) {
     const int mb = blockIdx.x;
     const int64_t n_in = a.in_count[mb];
     const int lc = a.chunk_size;
@@ -774,14 +763,13 @@ __global__ void __launch_bounds__(kTopkThreads) prune_topk_kernel(const hp_stage
     // pass finds the approximate K-th key, the chunks that bound cannot settle are replayed
     // exactly, and the second pass selects on settled keys
     const float bound = list_bound ? __uint_as_float(list_bound[2 * mb]) : 0.f;
-    extern __shared__ __align__(16) uint32_t topk_dyn[];  // refine: q rows of the heads, padded bf16
     const bool refine = keyed && bound > 0.f;
     uint32_t prefix = 0, pmask = 0;
     int need = static_cast<int>(K);
     for (int pass = 0; pass < (refine ? 2 : 1); ++pass) {
     if (pass == 1) {
         refine_band(a, mb, const_cast<float*>(sc), cc, key_to_float(prefix), 2.f * bound * 1.01f, list_bound[2 * mb + 1],
-                    topk_dyn, scan_tmp);
+                    reps, max_chunks, scan_tmp);
         prefix = 0; pmask = 0; need = static_cast<int>(K);
     }
     // Radix select (MSB first) of the K-th largest order key.
@@ -893,7 +881,8 @@ extern "C" size_t hp_stage_workspace_bytes(int32_t n_lists, int32_t max_chunks, 
     const size_t kmax = chunk_size > 0 ? static_cast<size_t>(keep / chunk_size) : 0;
     return align_up(static_cast<size_t>(n_lists) * max_chunks * 4, 256) +
            align_up(static_cast<size_t>(n_lists) * (kmax ? kmax : 1) * 4, 256) +
-           align_up(static_cast<size_t>(n_lists) * 8, 256) + 256;  // + per-list score bound, fp32-head mask
+           align_up(static_cast<size_t>(n_lists) * 8, 256) +                   // per-list score bound, fp32-head mask
+           align_up(static_cast<size_t>(n_lists) * max_chunks * kTcMaxHeads * 2, 256) + 256;  // rep offsets
 }
 
 template <typename T, int D, bool EXT>
@@ -922,7 +911,8 @@ static cudaError_t dispatch_descent(const hp_stage_args& a, float* scores, const
 static bool prune_uses_tc(const hp_stage_args& a) {
     const int rows_max = std::min(a.query_block, a.q_rows);
     return a.max_chunks > 0 && a.keys.dtype == HP_BF16 && a.keys.d == 128 && !a.rope.extension &&
-           a.keys_exact != nullptr && rows_max >= 16 && a.query_block <= 64 && a.heads_per_mask <= 8 &&
+           a.keys_exact != nullptr && rows_max >= 16 && a.query_block <= 64 && a.heads_per_mask <= kTcMaxHeads &&
+           a.chunk_size <= 65536 &&
            !hp_tc_descent_disabled();
 }
 
@@ -982,6 +972,8 @@ extern "C" int hp_prune_stage(const hp_stage_args* ap, void* stream) {
     uint32_t* list_bound = reinterpret_cast<uint32_t*>(
         ws + align_up(static_cast<size_t>(n_lists) * max_chunks * 4, 256) +
         align_up(static_cast<size_t>(n_lists) * (kmax ? kmax : 1) * 4, 256));
+    uint16_t* reps = reinterpret_cast<uint16_t*>(reinterpret_cast<char*>(list_bound) +
+                                                 align_up(static_cast<size_t>(n_lists) * 8, 256));
 
     hp_stage_args la = a;
     la.max_chunks = max_chunks;
@@ -999,7 +991,7 @@ extern "C" int hp_prune_stage(const hp_stage_args* ap, void* stream) {
                                                           static_cast<int>(kTcSmem)), "prune_descent_tc_kernel"))
             return rc;
         dim3 grid((max_chunks + 32 * kTcWarps - 1) / (32 * kTcWarps), a.heads_per_mask, n_lists);
-        kern<<<grid, kTcWarps * 32, kTcSmem, s>>>(la, reinterpret_cast<uint32_t*>(scores), list_bound, max_chunks);
+        kern<<<grid, kTcWarps * 32, kTcSmem, s>>>(la, reinterpret_cast<uint32_t*>(scores), list_bound, reps, max_chunks);
         if (int rc = hph::check_cuda(cudaGetLastError(), "prune_descent_tc_kernel")) return rc;
     } else if (a.max_chunks > 0) {
         StageGeom g{};
@@ -1020,13 +1012,8 @@ extern "C" int hp_prune_stage(const hp_stage_args* ap, void* stream) {
                                                       : dispatch_descent<float>(la, scores, g, s);
         if (int rc = hph::check_cuda(e, "prune_descent_kernel")) return rc;
     }
-    const size_t topk_smem = tc ? static_cast<size_t>(a.heads_per_mask) * 64 * kTcRow : 0;
-    if (tc && topk_smem > 48 * 1024)
-        if (int rc = hph::check_cuda(cudaFuncSetAttribute(prune_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                          static_cast<int>(topk_smem)), "prune_topk_kernel"))
-            return rc;
-    prune_topk_kernel<<<n_lists, kTopkThreads, topk_smem, s>>>(la, scores, sel, max_chunks, kmax, status, tc,
-                                                               tc ? list_bound : nullptr);
+    prune_topk_kernel<<<n_lists, kTopkThreads, 0, s>>>(la, scores, sel, max_chunks, kmax, status, tc,
+                                                        tc ? list_bound : nullptr, reps);
     return hph::check_cuda(cudaGetLastError(), "prune_topk_kernel");
 }
 
