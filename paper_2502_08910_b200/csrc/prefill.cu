@@ -15,7 +15,7 @@
 //   1. gather the K and V rows (16-byte cp.async through the page table) into the
 //      canonical no-swizzle UMMA layouts (K K-major, V MN-major), bf16;
 //   2. one thread issues S = Q K^T as 8 x tcgen05.mma (M=128, N=128, K=16) into TMEM;
-//   3. each thread owns one row: tcgen05.ld of its S row, causal/selection mask,
+//   3. four threads own a row (32 columns each): tcgen05.ld of their S columns, causal/selection mask,
 //      online-softmax update, P (bf16) to shared memory, O rescaled in TMEM
 //      (tcgen05.ld / tcgen05.st);
 //   4. O += P V as 8 x tcgen05.mma into the TMEM accumulator.
@@ -32,7 +32,9 @@ namespace {
 constexpr int kTM = 128;       // query rows per MMA tile (TMEM lanes)
 constexpr int kTN = 128;       // keys per tile
 constexpr int kHD = 128;       // head dim
-constexpr int kThreads = 256;  // two threads per query row (64 score columns each)
+constexpr int kThreads = 512;  // four threads per query row (32 score / output columns each)
+constexpr int kQ = kThreads / kTM;  // threads per row
+constexpr int kCols = kTN / kQ;     // score (and output) columns per thread
 constexpr uint32_t kTmemCols = 256;  // S [0,128) + O [128,256)
 
 // canonical no-swizzle layouts, byte offsets (8 x 16 B core matrices)
@@ -153,6 +155,7 @@ __global__ void __launch_bounds__(kThreads, 1) bsa_prefill_tc_kernel(const hp_bs
     __shared__ __align__(8) uint64_t bar_s, bar_o;
     __shared__ uint32_t tmem_base_sh;
     __shared__ int sh_counts[4];
+    static_assert(kCols == 32 && kTN == kHD, "a thread's S and O columns are one 32-column TMEM load each");
     using S = PrefillSmem;
     const int t = threadIdx.x, lane = t & 31, w = warp_id();
     const int bs = a.block_size;
@@ -225,14 +228,14 @@ __global__ void __launch_bounds__(kThreads, 1) bsa_prefill_tc_kernel(const hp_bs
         if (u >= st0 && u <= pos_last) uni[s0 + nmid + (u - st0)] |= static_cast<int32_t>(0x80000000u);
     }
     // ---- Q tile (bf16, K-major): tile row i = head (i / bs) of the pair, block row (i % bs)
-    const int my_i = t & (kTM - 1), half = t >> 7;  // row, score-column half
+    const int my_i = t & (kTM - 1), half = t >> 7;  // row, column quarter
     {
         const int i = my_i;
         const int hh = hp * hpt + i / bs, r = i % bs;
         const bool ok = r < rows_here;
         const float* qr = a.q + (static_cast<int64_t>(m * hpm + hh) * a.n_rows + row0 + r) * kHD;
         unsigned char* qs = smem + S::q_off;
-        for (int c = half * 8; c < half * 8 + 8; ++c) {
+        for (int c = half * (16 / kQ); c < (half + 1) * (16 / kQ); ++c) {
             uint4 pk = make_uint4(0, 0, 0, 0);
             if (ok) {
                 const float4 x0 = reinterpret_cast<const float4*>(qr)[2 * c];
@@ -251,15 +254,15 @@ __global__ void __launch_bounds__(kThreads, 1) bsa_prefill_tc_kernel(const hp_bs
     const bool all_see_low = pos_first + 1 >= s0;
     // softmax in base 2: scores scaled by log2(e)/sqrt(d), exponentials on MUFU.EX2
     const float scale = 1.4426950408889634f / sqrtf(static_cast<float>(kHD));
-    float run_m = -INFINITY, run_l = 0.f;  // run_l: this thread's half of the row sum
+    float run_m = -INFINITY, run_l = 0.f;  // run_l: this thread's quarter of the row sum
     const uint32_t lane_base = static_cast<uint32_t>((w & 3) * 32) << 16;
-    const uint32_t tS = tmem + lane_base + half * 64;        // this half's S columns
-    const uint32_t tO = tmem + lane_base + 128 + half * 64;  // this half's O columns
+    const uint32_t tS = tmem + lane_base + half * kCols;        // this quarter's S columns
+    const uint32_t tO = tmem + lane_base + 128 + half * kCols;  // this quarter's O columns
     const uint32_t idesc_qk = instr_desc(kTM, kTN, 0, 0);
     const uint32_t idesc_pv = instr_desc(kTM, kHD, 0, 1);
     const uint32_t sbase = smem_u32(smem);
     const int n_tiles = (U + kTN - 1) / kTN;
-    __shared__ float sh_max[2][kTM];
+    __shared__ float sh_max[kQ][kTM];
     // resident KV with power-of-two pages: a row is pool + 256 B x (page*n_kv + kvh)*ps + off,
     // 32-bit index math (rows < 2^32) instead of the general page-table walk
     const uint32_t ps = static_cast<uint32_t>(a.kv.page_size);
@@ -328,24 +331,23 @@ __global__ void __launch_bounds__(kThreads, 1) bsa_prefill_tc_kernel(const hp_bs
         progress(12 + tile * 10);
         tc_fence_after();
         // 4. masked online softmax over this thread's 64 columns; row max shared by the two halves
-        float sv[kTN / 2];
-#pragma unroll
-        for (int c = 0; c < kTN / 64; ++c) tmem_ld32(tS + c * 32, sv + c * 32);
+        float sv[kCols];
+        tmem_ld32(tS, sv);
         // selection test, branch-free (union entries past U read as 0x7fffffff = never
         // selected); four independent max chains
         float tm4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-        const int ub = tile * kTN + half * 64;
+        const int ub = tile * kTN + half * kCols;
         const int32_t pos32 = my_ok ? static_cast<int32_t>(my_pos) : -1;
         const int32_t sb32 = static_cast<int32_t>(my_sb), sink32 = static_cast<int32_t>(min64(sink, 0x7fffffff));
-        if (my_ok && all_see_low && ub + kTN / 2 <= s0 + nmid) {
+        if (my_ok && all_see_low && ub + kCols <= s0 + nmid) {
             // sinks and mask entries (union index < s0 + nmid) precede every row of the
             // block (< stream_begin(first row), and the first row already sees every
             // sink): all selected, no per-entry test
 #pragma unroll
-            for (int jj = 0; jj < kTN / 2; ++jj) tm4[jj & 3] = fmaxf(tm4[jj & 3], sv[jj]);
+            for (int jj = 0; jj < kCols; ++jj) tm4[jj & 3] = fmaxf(tm4[jj & 3], sv[jj]);
         } else {
 #pragma unroll
-        for (int j4 = 0; j4 < kTN / 2; j4 += 4) {  // four union entries per 16-byte load
+        for (int j4 = 0; j4 < kCols; j4 += 4) {  // four union entries per 16-byte load
             const int4 e4 = *reinterpret_cast<const int4*>(uni + ub + j4);
             const int32_t ev[4] = {e4.x, e4.y, e4.z, e4.w};
 #pragma unroll
@@ -365,14 +367,14 @@ __global__ void __launch_bounds__(kThreads, 1) bsa_prefill_tc_kernel(const hp_bs
         // lazy rescale (base 2): keep a stale running max unless the tile's max exceeds it
         // by more than 2^8 — P (bf16) and the fp32 sums stay in range, O and l share the
         // same reference, so the final O / l is unchanged; most tiles skip the TMEM rescale
-        const float tile_m = fmaxf(sh_max[0][my_i], sh_max[1][my_i]);
+        const float tile_m = fmaxf(fmaxf(sh_max[0][my_i], sh_max[1][my_i]), fmaxf(sh_max[2][my_i], sh_max[3][my_i]));
         const float new_m = (run_m != -INFINITY && tile_m <= run_m + 8.0f) ? run_m : fmaxf(run_m, tile_m);
         const float alpha = (run_m == -INFINITY) ? 0.f : ex2_approx(run_m - new_m);
         float ps4[4] = {0.f, 0.f, 0.f, 0.f};
         const float mref = new_m == -INFINITY ? 0.f : new_m;  // rows with nothing selected yet: all p = 0
         unsigned char* ps = smem + S::p_off;
 #pragma unroll
-        for (int c = 0; c < kTN / 16; ++c) {
+        for (int c = 0; c < kCols / 8; ++c) {
             float p[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
@@ -380,7 +382,7 @@ __global__ void __launch_bounds__(kThreads, 1) bsa_prefill_tc_kernel(const hp_bs
                 p[u] = ex2_approx(fmaf(x, scale, -mref));  // masked: ex2(-inf) = 0
                 ps4[u & 3] += p[u];
             }
-            *reinterpret_cast<uint4*>(ps + kmajor_off(my_i, half * 64 + c * 8)) =
+            *reinterpret_cast<uint4*>(ps + kmajor_off(my_i, half * kCols + c * 8)) =
                 make_uint4(pack_bf16(p[0], p[1]), pack_bf16(p[2], p[3]), pack_bf16(p[4], p[5]), pack_bf16(p[6], p[7]));
         }
         const float psum = (ps4[0] + ps4[1]) + (ps4[2] + ps4[3]);
@@ -389,13 +391,10 @@ __global__ void __launch_bounds__(kThreads, 1) bsa_prefill_tc_kernel(const hp_bs
         // tcgen05.ld/st are .sync.aligned: the whole warp rescales if any row needs it
         if (tile > 0 && __any_sync(0xffffffffu, alpha != 1.0f)) {
             float ov[32];
+            tmem_ld32(tO, ov);
 #pragma unroll
-            for (int c = 0; c < kHD / 64; ++c) {
-                tmem_ld32(tO + c * 32, ov);
-#pragma unroll
-                for (int u = 0; u < 32; ++u) ov[u] *= alpha;
-                tmem_st32(tO + c * 32, ov);
-            }
+            for (int u = 0; u < 32; ++u) ov[u] *= alpha;
+            tmem_st32(tO, ov);
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }
         fence_async_smem();
@@ -421,21 +420,17 @@ __global__ void __launch_bounds__(kThreads, 1) bsa_prefill_tc_kernel(const hp_bs
     }
     sh_max[half][my_i] = run_l;
     __syncthreads();
-    const float row_l = sh_max[0][my_i] + sh_max[1][my_i];
+    const float row_l = (sh_max[0][my_i] + sh_max[1][my_i]) + (sh_max[2][my_i] + sh_max[3][my_i]);
     {
         const int hh = hp * hpt + my_i / bs;
-        float* orow = a.out + (static_cast<int64_t>(m * hpm + hh) * a.n_rows + row0 + my_r) * kHD + half * 64;
+        float* orow = a.out + (static_cast<int64_t>(m * hpm + hh) * a.n_rows + row0 + my_r) * kHD + half * kCols;
         float ov[32];
+        if (n_tiles > 0) tmem_ld32(tO, ov);
+        if (my_ok) {
+            const float inv = row_l > 0.f ? 1.0f / row_l : NAN;
 #pragma unroll
-        for (int c = 0; c < kHD / 64; ++c) {
-            if (n_tiles > 0) tmem_ld32(tO + c * 32, ov);
-            if (my_ok) {
-                const float inv = row_l > 0.f ? 1.0f / row_l : NAN;
-#pragma unroll
-                for (int u = 0; u < 32; u += 4)
-                    *reinterpret_cast<float4*>(orow + c * 32 + u) =
-                        make_float4(ov[u] * inv, ov[u + 1] * inv, ov[u + 2] * inv, ov[u + 3] * inv);
-            }
+            for (int u = 0; u < 32; u += 4)
+                *reinterpret_cast<float4*>(orow + u) = make_float4(ov[u] * inv, ov[u + 1] * inv, ov[u + 2] * inv, ov[u + 3] * inv);
         }
     }
     tc_fence_before();
