@@ -336,6 +336,8 @@ typedef struct hp_decode_bsa_args {
     int32_t mask_stable;
 } hp_decode_bsa_args;
 
+/* The workspace starts with per-head-group last-CTA ticket counters: zero it once before
+ * first use (cudaMemset); every launch leaves the counters at zero for the next one. */
 size_t hp_decode_bsa_workspace_bytes(int32_t n_q_heads, int32_t max_sel);
 int hp_decode_bsa(const hp_decode_bsa_args* args, void* stream);
 
