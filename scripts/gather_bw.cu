@@ -65,6 +65,41 @@ __global__ void __launch_bounds__(128) gB(const char* buf, uint32_t nrows, int s
     if (acc == 12345.f) sink[0] = acc;
 }
 
+// D: the stage-1 descent pattern in the paged layout ([page][8 kv][64 tokens][256 B],
+// chunks of 256 tokens = 4 pages): lane = chunk, warp item = (chunk group, kv head), step
+// s visits token c*256 + a binary-search offset (the same for every chunk at the first
+// steps, then split by per-(chunk, head) random branch bits). skew: extra bytes per page
+// of pool stride (0 = the dense layout).
+__global__ void __launch_bounds__(128) gD(const char* buf, uint32_t n_chunks, int steps, uint32_t skew, float* sink) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    unsigned char* ks = sm + w * 32 * 256;
+    float acc = 0.f;
+    const uint32_t item = blockIdx.x * 4 + w;
+    const uint32_t kvh = item & 7, grp = item >> 3;
+    const uint32_t c = (grp * 32 + lane) % n_chunks;
+    const uint32_t bits = hash32(c * 8 + kvh + 12345);
+    const size_t page_stride = 8ull * 64 * 256 + skew;
+    uint32_t first = 0, half = 128;
+    for (int s = 0; s < steps; ++s) {
+        const uint32_t t = c * 256 + (s == 0 ? 0 : first + half);
+        if (s > 0) { if ((bits >> s) & 1) first += half; half >>= 1; if (half == 0) half = 1; }
+        const size_t off = (size_t)(t >> 6) * page_stride + ((size_t)kvh * 64 + (t & 63)) * 256;
+        unsigned long long p = (unsigned long long)(buf + off);
+        const int cc = lane & 15, sub = lane >> 4;
+        for (int r = 0; r < 32; r += 2) {
+            unsigned long long pp = __shfl_sync(0xffffffffu, p, r + sub);
+            cp16(ks + (r + sub) * 256 + ((cc ^ ((r + sub) & 15)) << 4), (const char*)pp + (cc << 4));
+        }
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
+        __syncwarp();
+        const uint4 v = *reinterpret_cast<const uint4*>(ks + lane * 256 + ((3 ^ (lane & 15)) << 4));
+        acc += __uint_as_float(v.x & 0x3fffffff) * 1e-30f;
+        __syncwarp();
+    }
+    if (acc == 12345.f) sink[0] = acc;
+}
+
 // C: streaming read (coalesced 16 B per lane)
 __global__ void gC(const uint4* buf, size_t n, float* sink) {
     uint32_t acc = 0;
@@ -111,6 +146,22 @@ int main() {
             float ms; cudaEventElapsedTime(&ms, a, b); if (ms < best) best = ms;
         }
         printf("%s unloaded: %.0f ns per gather step\n", v ? "bulk " : "cpasync", best * 1e6 / 64);
+    }
+    // descent pattern: 4,096 chunks (1M tokens) x 8 kv heads = 1,024 warps of 32 chunks x 8 heads... one wave
+    cudaFuncSetAttribute(gD, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 32 * 256);
+    for (uint32_t skew : {0u, 256u, 512u, 1024u, 4096u}) {
+        const uint32_t n_chunks = 4096;  // 1M tokens: 16,384 pages x (128 KB + skew) < 2 GB
+        const int grid = n_chunks / 32 * 8 / 4;  // 1,024 warps of (32 chunks, 1 head) per kv head pass
+        float best = 1e9;
+        for (int rep = 0; rep < 5; ++rep) {
+            cudaEventRecord(a);
+            for (int k = 0; k < 4; ++k) gD<<<grid, 128, 4 * 32 * 256>>>(buf, n_chunks, 9, skew, sink);  // 4 q-heads per kv head
+            cudaEventRecord(b); cudaEventSynchronize(b);
+            float ms; cudaEventElapsedTime(&ms, a, b); if (ms < best) best = ms;
+        }
+        double moved = 4.0 * grid * 128 * 9 * 256;
+        printf("descent pattern skew %4u B/page: %.1f us, %.0f GB/s  err=%s\n", skew, best * 1e3, moved / (best * 1e-3) / 1e9,
+               cudaGetErrorString(cudaGetLastError()));
     }
     for (int rep = 0; rep < 3; ++rep) {
         cudaEventRecord(a);
