@@ -150,7 +150,7 @@ int main() {
     // descent pattern: 4,096 chunks (1M tokens) x 8 kv heads = 1,024 warps of 32 chunks x 8 heads... one wave
     cudaFuncSetAttribute(gD, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 32 * 256);
     for (uint32_t skew : {0u, 256u, 512u, 1024u, 4096u}) {
-        const uint32_t n_chunks = 4096;  // 1M tokens: 16,384 pages x (128 KB + skew) < 2 GB
+        const uint32_t n_chunks = 3700;  // ~0.95M tokens: 14,800 pages x (128 KB + skew) < 2 GB
         const int grid = n_chunks / 32 * 8 / 4;  // 1,024 warps of (32 chunks, 1 head) per kv head pass
         float best = 1e9;
         for (int rep = 0; rep < 5; ++rep) {
