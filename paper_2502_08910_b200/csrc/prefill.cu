@@ -45,7 +45,9 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
     return r;
 }
 
-// dev: progress codes written by thread 0 to a (mapped host) word, to locate a stall
+// dev builds: progress codes written by thread 0 to a (mapped host) word, to locate a
+// stall; compiled out of the product kernel
+#if defined(HP_TRACE) || defined(HP_DEV)
 __device__ volatile int* g_pf_progress = nullptr;
 __device__ __forceinline__ void progress(int code) {
     if (threadIdx.x == 0 && g_pf_progress) {
@@ -53,6 +55,9 @@ __device__ __forceinline__ void progress(int code) {
         __threadfence_system();
     }
 }
+#else
+__device__ __forceinline__ void progress(int) {}
+#endif
 
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;
