@@ -308,6 +308,7 @@ def run_step(layer: SeqShardLayer, pos: int, group=None) -> torch.Tensor:
     per stage an all-gather of chunk scores + chunk counts, then one of the (m, l, o)
     partials. Every rank returns the merged output [n_q_heads, 128]."""
     world = layer.geo.world
+    layer._keep.clear()  # the previous step's launch arguments (stream order keeps them valid)
     for i in range(len(layer.stages)):
         sc, cnt = layer.descend(i, pos)
         layer.select(i, _all_gather(sc, world, group), _all_gather(cnt, world, group))
@@ -320,6 +321,8 @@ def run_step(layer: SeqShardLayer, pos: int, group=None) -> torch.Tensor:
 def run_step_virtual(layers: list[SeqShardLayer], pos: int) -> torch.Tensor:
     """The same step with every shard in this process (single-GPU parity check): the
     collectives become stacks of the shards' tensors."""
+    for ly in layers:
+        ly._keep.clear()
     for i in range(len(layers[0].stages)):
         outs = [ly.descend(i, pos) for ly in layers]
         g_sc = torch.stack([sc for sc, _ in outs])
