@@ -46,7 +46,8 @@ constexpr int kSlot = 32 * kRow;                      // one 32-row staging slot
 constexpr int kTile = 256;                            // attention keys per tile (K + V = 128 KB)
 constexpr int kTileKV = 2 * kTile * kRow;             // 128 KB
 // 140 KB: 16 warps x 8 KB of descent staging, or the attention tile + row pointers + p
-constexpr int kStageBytes = kTileKV + 2 * kTile * 8 + 8 * kTile * 4;
+constexpr int kPw = kTile + 8;                        // p row stride (floats): head rows 8 banks apart
+constexpr int kStageBytes = kTileKV + 2 * kTile * 8 + 8 * kPw * 4;
 constexpr int kMaxS = 4;
 constexpr int kPart = kD + 2;                         // partial record: o[128], m, l
 constexpr int kKeysMax = 16384;                       // chunk keys per stage selection
@@ -74,14 +75,15 @@ struct LayerParams {
 // warp), the selection's key copy (offset 0), the attention tile (K/V at 0, row pointers
 // and probabilities behind it), the merge's staged partials; then the small arrays.
 struct LayerSmem {
-    size_t ptrs, pw, sel, qs, qb, red, part, bytes;
+    size_t ptrs, pw, sel, qs, qb, qf, red, part, bytes;
     __host__ __device__ LayerSmem(int sel_total, int hp, int red_cap) {
         ptrs = kTileKV;                                      // K and V row pointers [2][kTile]
-        pw = ptrs + 2 * kTile * 8;                           // [hp][kTile] scores / probabilities
+        pw = ptrs + 2 * kTile * 8;                           // [hp][kPw] scores / probabilities
         size_t o = kStageBytes;
         sel = o; o += align_up(static_cast<size_t>(sel_total) * 4, 16);
         qs = o; o += static_cast<size_t>(hp) * kD * 4;
         qb = o; o += static_cast<size_t>(hp) * kD * 2;
+        qf = o; o += 8 * 2 * 2 * 32 * 4;                     // QK^T A fragments [k-step][half][hi, lo][lane]
         red = o; o += align_up(static_cast<size_t>(hp) * red_cap * 4, 16);
         part = o; o += align_up(static_cast<size_t>(hp) * kPart * 4, 16);
         bytes = o;
@@ -144,6 +146,7 @@ __global__ void __launch_bounds__(kLT, 1) decode_layer_kernel(const LayerParams 
     int32_t* sel = reinterpret_cast<int32_t*>(smem + L.sel);
     float* qs = reinterpret_cast<float*>(smem + L.qs);
     uint32_t* qb = reinterpret_cast<uint32_t*>(smem + L.qb);
+    uint32_t* qfr = reinterpret_cast<uint32_t*>(smem + L.qf);
     float* red = reinterpret_cast<float*>(smem + L.red);
     float* part = reinterpret_cast<float*>(smem + L.part);
     const int kvh = (m * HP) / (a.n_q_heads / a.kv.n_kv);  // the mask's heads share one kv head (host-checked)
@@ -162,6 +165,15 @@ __global__ void __launch_bounds__(kLT, 1) decode_layer_kernel(const LayerParams 
     const bool use_fma = __syncthreads_and(safe) && a.keys_exact != nullptr && *a.keys_exact != 0;
     for (int i = t; i < HP * kD / 2; i += kLT)
         qb[i] = (__float_as_uint(qs[2 * i]) >> 16) | (__float_as_uint(qs[2 * i + 1]) & 0xffff0000u);
+    // the attention's QK^T A fragments (rows = heads, bf16 hi + lo parts of q), built once
+    for (int i = t; i < 8 * 2 * 32; i += kLT) {
+        const int ks = i >> 6, half = (i >> 5) & 1, ln = i & 31, gg = ln >> 2, tt = ln & 3;
+        const int d = ks * 16 + half * 8 + 2 * tt;
+        const float x0 = gg < HP ? qs[gg * kD + d] : 0.f, x1 = gg < HP ? qs[gg * kD + d + 1] : 0.f;
+        const uint32_t h2 = pack_bf16(x0, x1);
+        qfr[((ks * 2 + half) * 2) * 32 + ln] = h2;
+        qfr[((ks * 2 + half) * 2 + 1) * 32 + ln] = pack_bf16(x0 - bf16_lo(h2), x1 - bf16_hi(h2));
+    }
 
     // the attention's sink and stream rows are known now: warm them into L2 while the
     // stages run (the group's CTAs split them; K and V, two 128 B lines per row)
@@ -447,30 +459,26 @@ __global__ void __launch_bounds__(kLT, 1) decode_layer_kernel(const LayerParams 
         if (pt == p0) trace(21, 2);
         // S = q K^T: warp w takes key tiles of 8 (n = key), 8 k-steps, hi and lo q
         for (int kt = w; kt < nk16 / 8; kt += kLW) {
-            float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
+            float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;  // hi parts of q
+            float e0 = 0.f, e1 = 0.f, e2 = 0.f, e3 = 0.f;  // lo parts: an independent MMA chain
             const int j = kt * 8 + g;  // this thread's key for the B fragment
             const unsigned char* kr = Ks + j * kRow;
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks) {
-                uint32_t ah[2], al[2];
-#pragma unroll
-                for (int half = 0; half < 2; ++half) {
-                    const int d = ks * 16 + half * 8 + 2 * tq;
-                    const float x0 = g < HP ? qs[g * kD + d] : 0.f, x1 = g < HP ? qs[g * kD + d + 1] : 0.f;
-                    const uint32_t h2 = pack_bf16(x0, x1);
-                    ah[half] = h2;
-                    al[half] = pack_bf16(x0 - bf16_lo(h2), x1 - bf16_hi(h2));
-                }
+                const uint32_t ah0 = qfr[((ks * 2 + 0) * 2) * 32 + lane], al0 = qfr[((ks * 2 + 0) * 2 + 1) * 32 + lane];
+                const uint32_t ah1 = qfr[((ks * 2 + 1) * 2) * 32 + lane], al1 = qfr[((ks * 2 + 1) * 2 + 1) * 32 + lane];
                 const int d0 = ks * 16 + 2 * tq, d1 = d0 + 8;
                 const uint32_t b0 = *reinterpret_cast<const uint32_t*>(kr + (((d0 >> 3) ^ (j & 15)) << 4) + (d0 & 7) * 2);
                 const uint32_t b1 = *reinterpret_cast<const uint32_t*>(kr + (((d1 >> 3) ^ (j & 15)) << 4) + (d1 & 7) * 2);
-                mma_bf16_16816(c0, c1, c2, c3, ah[0], ah[1], b0, b1);
-                mma_bf16_16816(c0, c1, c2, c3, al[0], al[1], b0, b1);
+                mma_bf16_16816(c0, c1, c2, c3, ah0, ah1, b0, b1);
+                mma_bf16_16816(e0, e1, e2, e3, al0, al1, b0, b1);
             }
+            c0 += e0;
+            c1 += e1;
             if (g < HP) {
                 const int jj = kt * 8 + 2 * tq;
-                pw[g * kTile + jj] = jj < nk ? c0 * scale : -INFINITY;
-                pw[g * kTile + jj + 1] = jj + 1 < nk ? c1 * scale : -INFINITY;
+                pw[g * kPw + jj] = jj < nk ? c0 * scale : -INFINITY;
+                pw[g * kPw + jj + 1] = jj + 1 < nk ? c1 * scale : -INFINITY;
             }
         }
         __syncthreads();
@@ -478,15 +486,15 @@ __global__ void __launch_bounds__(kLT, 1) decode_layer_kernel(const LayerParams 
         // online softmax per head: warp h reduces head h's tile
         if (w < HP) {
             float mt = -INFINITY;
-            for (int j = lane; j < nk; j += 32) mt = fmaxf(mt, pw[w * kTile + j]);
+            for (int j = lane; j < nk; j += 32) mt = fmaxf(mt, pw[w * kPw + j]);
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, o));
             const float m_old = sh_m[w];
             const float m_new = fmaxf(m_old, mt);
             float ls = 0.f;
             for (int j = lane; j < nk16; j += 32) {
-                const float p = j < nk ? expf(pw[w * kTile + j] - m_new) : 0.f;
-                pw[w * kTile + j] = p;
+                const float p = j < nk ? expf(pw[w * kPw + j] - m_new) : 0.f;
+                pw[w * kPw + j] = p;
                 ls += p;
             }
 #pragma unroll
@@ -513,7 +521,7 @@ __global__ void __launch_bounds__(kLT, 1) decode_layer_kernel(const LayerParams 
 #pragma unroll
                 for (int half = 0; half < 2; ++half) {
                     const int kk = k0 + half * 8 + 2 * tq;
-                    const float p0_ = g < HP ? pw[g * kTile + kk] : 0.f, p1_ = g < HP ? pw[g * kTile + kk + 1] : 0.f;
+                    const float p0_ = g < HP ? pw[g * kPw + kk] : 0.f, p1_ = g < HP ? pw[g * kPw + kk + 1] : 0.f;
                     const uint32_t h2 = pack_bf16(p0_, p1_);
                     ah[half] = h2;
                     alo[half] = pack_bf16(p0_ - bf16_lo(h2), p1_ - bf16_hi(h2));
