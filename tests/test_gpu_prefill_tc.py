@@ -183,3 +183,21 @@ def test_tc_descent_equals_cuda_core_at_c4(tmp_path):
     for g in range(c.shape[0]):
         for b in range(c.shape[1]):
             assert np.array_equal(lt[g, b, : c[g, b]], lc[g, b, : c[g, b]]), (g, b)
+
+
+@pytest.mark.parametrize("t_kv,t_q,stages", [
+    (8192, 500, [(64, 64, 2048), (64, 16, 512), (64, 4, 256)]),   # last block: 52 rows
+    (6000, 333, [(32, 32, 1024), (32, 8, 256), (16, 4, 128)]),    # b_q 32 -> 16 remap, ragged tail
+    (9000, 777, [(64, 128, 4096), (32, 16, 512)]),                # 128-token chunks, ragged everything
+])
+def test_tc_descent_ragged_blocks_exact(port, t_kv, t_q, stages):
+    """Tensor-core descent at ragged shapes: a short last query block (fewer q rows than the
+    MMA's n-tiles), b_q = 32 and 16 (rows >= 16 still take the tensor cores), a sub-block
+    remap between stages, a context that is no multiple of the chunk size."""
+    D = _D()
+    from paper_2502_08910_b200 import synth
+    groups, hpm = 2, 4
+    q, k, _ = synth.generate(groups * hpm, groups, t_kv, 128, t_q=t_q, seed=t_q)
+    D.PRUNE_VARIANTS_USED.clear()
+    _masks_vs_oracle(port, D, q, k, stages, 128, 512, groups, hpm)
+    assert 1 in set(D.PRUNE_VARIANTS_USED)
