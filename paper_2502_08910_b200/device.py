@@ -560,11 +560,17 @@ class FusedDecodeLayer:
             a.cache[i], a.cache_stride[i] = _ptr(self.cache[i]), self.cache[i].shape[-1]
         a.n_masks, a.heads_per_mask, a.n_q_heads = self.n_masks, self.hpm, self.n_q_heads
         a.sink_tokens, a.stream_tokens = self.sink, self.stream_tokens
-        a.q, a.query_position, a.out = _ptr(self.q), t - 1, _ptr(self.out)
+        a.q, a.query_position, a.out = _ptr(self.q), t - 1, self._out_ptr()
         a.workspace, a.workspace_bytes = _ptr(self.ws_stage), self.ws_stage.numel()
         a.kv = self.kv.view(t)
         a.keys_exact = _ptr(self.kv.keys_exact)
         return a
+
+    def _out_ptr(self) -> int:
+        """Where the step's output goes: self.out, or (inside step_host graphs) the pinned
+        host buffer itself — the merging CTA stores straight to host memory (UVA), so the
+        host-facing call needs no device-to-host copy."""
+        return getattr(self, "_out_override", None) or _ptr(self.out)
 
     def fused_supported(self) -> bool:
         """hp_decode_layer takes this configuration (bf16, d = 128, RoPE extension off,
@@ -633,7 +639,7 @@ class FusedDecodeLayer:
             n_q_heads=self.n_q_heads, heads_per_mask=self.hpm, sink_tokens=self.sink,
             stream_tokens=self.stream_tokens, q=_ptr(self.q), query_position=pos,
             mask=chains[-1], mask_count=_ptr(self.count[-1]), max_mask=self.stages[-1][2],
-            out=_ptr(self.out), part_m=None, part_l=None, part_o=None,
+            out=self._out_ptr(), part_m=None, part_l=None, part_o=None,
             workspace=_ptr(self.ws_bsa), workspace_bytes=self.ws_bsa.numel(), kv=kvv,
             rope=self.policy.ctx(0, self.rope),
             # the last stage's cache is untouched this step: gather in the PDL prologue
@@ -698,7 +704,8 @@ class FusedDecodeLayer:
         """The host-facing decode call for the token at position t-1 (what a serving
         loop calls per layer): host q [n_q_heads, d] fp32 and the token's K/V rows
         [n_kv, d] in, host output [n_q_heads, d] fp32 out. One CUDA graph per
-        (t, refresh): pinned H2D copy -> append kernel -> the layer step -> D2H copy.
+        (t, refresh): pinned H2D copy -> append kernel -> the layer step, whose merging CTA
+        stores the output straight into the pinned host buffer (no D2H copy).
         Returns the pinned output buffer (valid after sync)."""
         has_kv = k_row is not None
         key = (t, tuple(refresh) if refresh is not None else None, has_kv)
@@ -718,7 +725,7 @@ class FusedDecodeLayer:
         if g is None:
             def body():
                 # one H2D copy of q + the token's K/V rows, append, the layer step (stage
-                # caches materialized on a side branch), one D2H copy of the output
+                # caches materialized on a side branch; output written to host memory)
                 cur = torch.cuda.current_stream()
                 n_in = self._d_io.numel() if has_kv else self._io_q
                 self._d_io[:n_in].copy_(self._h_io[:n_in], non_blocking=True)
@@ -728,8 +735,11 @@ class FusedDecodeLayer:
                                                  t - 1, _ptr(self.kv.keys_exact),
                                                  C.c_void_p(_stream())))
                 self._side.wait_stream(cur)
-                self.run(t, refresh=refresh, mat_stream=self._side)
-                self._h_out.copy_(self.out, non_blocking=True)
+                self._out_override = self._h_out.data_ptr()  # output stored to pinned host memory
+                try:
+                    self.run(t, refresh=refresh, mat_stream=self._side)
+                finally:
+                    self._out_override = None
                 cur.wait_stream(self._side)
             s = torch.cuda.Stream(device=self.dev)
             s.wait_stream(torch.cuda.current_stream())

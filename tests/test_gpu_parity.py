@@ -344,7 +344,8 @@ def test_fused_decode_refresh_schedule():
 
 def test_fused_step_host_matches_device_path():
     """The host-facing per-layer call (pinned q/K/V in, one H2D copy, append, step with
-    side-branch caches, one D2H copy) equals the device path driven step by step."""
+    side-branch caches, output stored by the kernel into the pinned host buffer) equals the
+    device path driven step by step."""
     D = _dev()
     dev = torch.device("cuda")
     stages = [(1, 64, 4096), (1, 16, 1024), (1, 4, 256)]
