@@ -18,7 +18,8 @@
 //     and writes the chunk keys (max over the group's heads, order-mapped) to L2;
 //   * one group barrier, every CTA copies the full key set and runs the same exact
 //     radix top-K, so all hold the kept chunk ids and resolve the next stage's input
-//     through shared memory;
+//     through shared memory (stage 0's keys need no exchange: every CTA forms them from
+//     the descent kernel's L2-resident scores, so that selection has no barrier);
 //   * the attention splits the selected positions over the CTAs (K/V gathered by
 //     cp.async, QK^T and PV on mma.sync with bf16 hi/lo splits of q and p), the sink and
 //     stream rows having been prefetched into L2 while the stages ran; partials (m, l, o)
@@ -230,20 +231,30 @@ __global__ void __launch_bounds__(kLT, 1) decode_layer_kernel(const LayerParams 
         } else {
             if (i == 1) trace(22, 0);
             if (i == 0) {
-                // stage 0's scores (decode.cu descent kernels): this CTA's slice, max over heads
-                const int64_t per = (cc + CS - 1) / CS;
-                const int64_t c0 = static_cast<int64_t>(rank) * per, c1 = min64(cc, c0 + per);
-                for (int64_t c = c0 + t; c < c1; c += kLT) {
-                    float v[8];
+                // stage 0's scores (decode.cu descent kernels, L2-resident): every CTA reads all
+                // of them and forms the keys itself (max over heads) — no key exchange and no
+                // group barrier for this selection
+                for (int64_t c0 = 0; c0 < cc; c0 += 2 * kLT) {
+                    float v[2][8];
 #pragma unroll
-                    for (int h = 0; h < 8; ++h)  // every plane's load in flight before the first use
-                        v[h] = h < P.planes0 ? __ldcg(P.scores0 + (static_cast<int64_t>(m) * P.planes0 + h) * P.max_chunks0 + c)
-                                             : -INFINITY;
-                    float best = -INFINITY;
+                    for (int u = 0; u < 2; ++u) {
+                        const int64_t c = c0 + u * kLT + t;
 #pragma unroll
-                    for (int h = 0; h < 8; ++h) best = (best < v[h]) ? v[h] : best;  // std::max in head order (pruning.cpp:182)
-                    put_key(c, order_key(best));
+                        for (int h = 0; h < 8; ++h)  // every plane's load in flight before the first use
+                            v[u][h] = (c < cc && h < P.planes0)
+                                          ? __ldcg(P.scores0 + (static_cast<int64_t>(m) * P.planes0 + h) * P.max_chunks0 + c)
+                                          : -INFINITY;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const int64_t c = c0 + u * kLT + t;
+                        float best = -INFINITY;
+#pragma unroll
+                        for (int h = 0; h < 8; ++h) best = (best < v[u][h]) ? v[u][h] : best;  // std::max in head order (pruning.cpp:182)
+                        if (c < cc) keys[c] = order_key(best);
+                    }
                 }
+                __syncthreads();
             } else if (lc <= 8 && 32 % lc == 0) {
                 // short chunks: a warp item = 32 / lc whole chunks, lane = row; one gather for
                 // all heads, each head's Alg. 3 descent replayed on the row scores with shuffles
@@ -375,30 +386,32 @@ __global__ void __launch_bounds__(kLT, 1) decode_layer_kernel(const LayerParams 
                     }
                 }
             }
-            if (i == 1) trace(22, 1);
-            group_barrier(gbar, static_cast<int>(++n_bar * CS));  // every CTA's keys are in L2
-            if (i == 1) trace(22, 2);
-            const uint32_t* gk = P.gkeys + (static_cast<size_t>(buf) * a.n_masks + m) * P.keys_cap;
-            for (int64_t j0 = 0; j0 < cc; j0 += 8 * kLT) {  // 8 independent loads in flight per thread
-                uint32_t v[8];
+            if (i != 0) {
+                if (i == 1) trace(22, 1);
+                group_barrier(gbar, static_cast<int>(++n_bar * CS));  // every CTA's keys are in L2
+                if (i == 1) trace(22, 2);
+                const uint32_t* gk = P.gkeys + (static_cast<size_t>(buf) * a.n_masks + m) * P.keys_cap;
+                for (int64_t j0 = 0; j0 < cc; j0 += 8 * kLT) {  // 8 independent loads in flight per thread
+                    uint32_t v[8];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int64_t j = j0 + u * kLT + t;
-                    v[u] = j < cc ? __ldcg(gk + j) : 0u;
-                }
+                    for (int u = 0; u < 8; ++u) {
+                        const int64_t j = j0 + u * kLT + t;
+                        v[u] = j < cc ? __ldcg(gk + j) : 0u;
+                    }
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int64_t j = j0 + u * kLT + t;
-                    if (j < cc) keys[j] = v[u];
+                    for (int u = 0; u < 8; ++u) {
+                        const int64_t j = j0 + u * kLT + t;
+                        if (j < cc) keys[j] = v[u];
+                    }
                 }
+                __syncthreads();
             }
-            __syncthreads();
             if (i == 1) trace(22, 3);
             cta_topk_smem(keys, static_cast<int>(cc), K, seli, tsh);
             if (i == 1) trace(22, 4);
             n_out = static_cast<int64_t>(K - 1) * lc + min64(lc, n_in - static_cast<int64_t>(seli[K - 1]) * lc);
             n_sel = K;
-            buf ^= 1;  // a fast CTA's next keys never land in a buffer a slow CTA still copies
+            if (i != 0) buf ^= 1;  // a fast CTA's next keys never land in a buffer a slow CTA still copies
         }
         if (rank == 0) {  // the stage's kept chunk ids and output length (the caches' source)
             for (int j = t; j < n_sel; j += kLT) a.sel[i][static_cast<int64_t>(m) * a.sel_stride[i] + j] = seli[j];
