@@ -392,6 +392,10 @@ size_t hp_decode_layer_workspace_bytes(int32_t n_masks, int32_t max_chunks0);
 /* 1 when hp_decode_layer takes this configuration, 0 otherwise (then use the
  * per-stage entry points); no launch. */
 int hp_decode_layer_supported(const hp_decode_layer_args* args);
+/* The layer kernel is a persistent grid (one CTA per SM, the CTAs of a KV group meeting at
+ * barriers in L2): do not run two hp_decode_layer launches concurrently on one device
+ * (different streams of one context) — each could hold SMs the other's barriers wait for.
+ * Stream-ordered launches (one stream, or graphs) and other kernels alongside are fine. */
 int hp_decode_layer(const hp_decode_layer_args* args, void* stream);
 
 /* Append one token's K/V rows (DecodeEngine::step, decode.cpp:202-208): rows
