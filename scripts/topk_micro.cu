@@ -185,11 +185,15 @@ int main() {
         for (int i = 0; i < n; ++i) { float s = 0; for (int k = 0; k < 12; ++k) s += rand() / (float)RAND_MAX; h[i] = (s - 6.0f) * 3.0f; }
         cudaMemcpy(d, h, n * 4, cudaMemcpyHostToDevice);
         cudaFuncSetAttribute(prof, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        prof<<<1, 512, smem>>>(d, 1024, 256, po);
-        long long r[32]; cudaMemcpy(r, po, 256, cudaMemcpyDeviceToHost);
-        printf("phase stamps (cycles): ");
-        for (int i = 0; i < 32; ++i) if (i == 0 || r[i]) printf("%lld ", r[i]);
-        printf("\n");
+        for (int cfg2 = 0; cfg2 < 2; ++cfg2) {
+            const int cc2 = cfg2 ? 4091 : 1024, k2 = cfg2 ? 128 : 256;
+            cudaMemset(po, 0, 512);
+            prof<<<1, 512, smem>>>(d, cc2, k2, po);
+            long long r[32]; cudaMemcpy(r, po, 256, cudaMemcpyDeviceToHost);
+            printf("phase stamps cc=%d K=%d (cycles): ", cc2, k2);
+            for (int i = 0; i < 32; ++i) if (i == 0 || r[i]) printf("%lld ", r[i]);
+            printf("\n");
+        }
     }
     return 0;
 }
