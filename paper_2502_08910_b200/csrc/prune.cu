@@ -347,8 +347,9 @@ __global__ void __launch_bounds__(256) prune_descent_kernel(const hp_stage_args 
 // the whole warp on one row), so every branch decision is the reference's. The chunk
 // keys (max over the heads, order keys, atomicMax) stay approximate with the list's
 // bound; prune_topk_kernel keeps the chunks certainly above the K-th key, drops those
-// certainly below, and replays the descents of the few in between exactly
-// (pruning.cpp:69-98,170-192). One CTA per (mask-block, head, 256 chunks).
+// certainly below, and scores the representatives of the few in between exactly (the
+// descent records each head's representative) (pruning.cpp:69-98,170-192). One CTA per
+// (mask-block, head, 256 chunks).
 constexpr int kTcRow = 272;                   // padded bf16 row (ldmatrix rows hit distinct banks)
 constexpr int kTcWarps = 8;
 constexpr int kTcQBytes = 64 * 128 * 4;       // fp32 q rows (fallback) or padded bf16 q rows
@@ -620,7 +621,7 @@ __global__ void __launch_bounds__(kTcWarps * 32, 2) prune_descent_tc_kernel(cons
         }
     }
     // approximate chunk key (max over the heads) and the list's bound; prune_topk_kernel
-    // certifies the kept set and replays the chunks near its boundary exactly
+    // certifies the kept set and rescores the chunks near its boundary exactly
     if (active) {
         atomicMax(keys_out + static_cast<int64_t>(mb) * max_chunks + j, order_key(s1));  // max over heads (pruning.cpp:182)
         rep_out[(static_cast<int64_t>(mb) * max_chunks + j) * kTcMaxHeads + hh] = static_cast<uint16_t>(first - 1);
@@ -760,7 +761,7 @@ __global__ void __launch_bounds__(kTopkThreads, 2) prune_topk_kernel(const hp_st
     __shared__ int sh_above;
 
     // keys from the tensor-core descent are approximate within the list's bound: the first
-    // pass finds the approximate K-th key, the chunks that bound cannot settle are replayed
+    // pass finds the approximate K-th key, the chunks that bound cannot settle are rescored
     // exactly, and the second pass selects on settled keys
     const float bound = list_bound ? __uint_as_float(list_bound[2 * mb]) : 0.f;
     const bool refine = keyed && bound > 0.f;
